@@ -1,0 +1,281 @@
+/* gnna.h — the C-ABI boundary of the B200 GNNAdvisor aggregation runtime.
+ *
+ * Plain pointers and sizes only: no C++ or torch types cross this line.  Every
+ * device-pointer entry point is stream-ordered on the context's stream
+ * (gnna_set_stream; default: the legacy default stream) and returns without
+ * synchronising unless it returns a host scalar.  Each entry names the
+ * reference interface (/root/reference/proj, namespace gnnsim) it replaces;
+ * the C++ drop-in (the include/gnnsim/ headers, libgnnsim_b200.so) is implemented on
+ * top of exactly these calls.
+ *
+ * Errors mirror the reference's exception taxonomy (error.hpp:9-38):
+ * GNNA_ERR_DOMAIN <-> DomainError (with the reference's message text),
+ * GNNA_ERR_INTERNAL <-> InternalError.  CUDA/OOM failures have their own
+ * codes.  gnna_last_error(ctx) returns the message of the last failure on ctx.
+ *
+ * There is no CPU fallback: every compute entry point runs CUDA kernels built
+ * for sm_100a; without a usable device gnna_create fails with GNNA_ERR_CUDA.
+ */
+#ifndef GNNA_H
+#define GNNA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GNNA_API __attribute__((visibility("default")))
+#else
+#define GNNA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int gnna_status;
+#define GNNA_OK 0
+#define GNNA_ERR_DOMAIN 1
+#define GNNA_ERR_INTERNAL 2
+#define GNNA_ERR_CUDA 3
+#define GNNA_ERR_OOM 4
+
+/* engine.hpp:21 Strategy */
+#define GNNA_NAIVE_ATOMIC 0
+#define GNNA_UNIT_SYNC 1
+#define GNNA_WARP_SHARED 2
+/* schedule.hpp:42 DimMode */
+#define GNNA_DIM_SEQUENTIAL 0
+#define GNNA_DIM_CYCLIC 1
+/* element type of feature matrices */
+#define GNNA_F32 0
+#define GNNA_F64 1
+
+/* schedule.hpp:14-27 KernelParams (same field meaning; tpw fixed at 32). */
+typedef struct {
+    uint32_t ngs, dw, tpb, tpw, dim;
+} gnna_params;
+
+/* engine.hpp:30-53 CostReport */
+typedef struct {
+    uint64_t atomic_ops, global_reads, global_writes, global_transactions;
+    uint64_t shared_bytes_per_block, cache_hits, cache_accesses;
+} gnna_cost;
+
+/* decider.hpp:12-26 ModelInputs (field order is the ABI). */
+typedef struct {
+    uint64_t num_nodes, num_edges;
+    uint32_t dim, max_tpb;
+    double avg_degree, stddev_degree;
+    uint64_t smem_per_block, capability;
+    double alpha;
+} gnna_model_inputs;
+
+typedef struct gnna_ctx gnna_ctx;
+typedef struct gnna_plan gnna_plan;
+
+/* ------------------------------------------------------------ context --- */
+GNNA_API gnna_status gnna_create(int device, gnna_ctx** out);
+GNNA_API void gnna_destroy(gnna_ctx* ctx);
+GNNA_API gnna_status gnna_set_stream(gnna_ctx* ctx, void* cuda_stream);
+GNNA_API void* gnna_get_stream(const gnna_ctx* ctx);
+GNNA_API gnna_status gnna_synchronize(gnna_ctx* ctx);
+GNNA_API const char* gnna_last_error(const gnna_ctx* ctx);
+GNNA_API const char* gnna_version(void);
+/* Number of kernels this library has launched on ctx (for bench.py). */
+GNNA_API uint64_t gnna_launch_count(const gnna_ctx* ctx);
+
+/* -------------------------------------------------- parameter domain --- */
+/* schedule.cpp:7-14 KernelParams::validate — same order, same messages. */
+GNNA_API gnna_status gnna_validate_params(gnna_ctx* ctx, const gnna_params* p);
+
+/* ------------------------------------------------ preprocessing (K1/K2) */
+/* Number of workload units: sum_v ceil(deg(v)/ngs) (schedule.cpp:16-30). */
+GNNA_API gnna_status gnna_count_groups(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
+                              uint32_t ngs, uint64_t* num_groups);
+/* schedule.hpp:76 partition_neighbors: unit u covers CSR range
+ * [d_part_ptr[u], d_part_ptr[u+1]) of node d_part2node[u] (NeighborGroup
+ * {id=u, target, begin, end}; begin_{u+1} == end_u, so G+1 offsets suffice). */
+GNNA_API gnna_status gnna_partition_neighbors(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
+                                     uint32_t ngs, uint64_t* d_part_ptr,
+                                     uint32_t* d_part2node);
+/* memplan.hpp:43 build_mem_plan (Algorithm 1) for warps targeting
+ * d_part2node[0..G): slot (node_shared_addr, slot index) and leader
+ * (unit_leader) per unit.  GNNA_ERR_DOMAIN when a node's units are not
+ * consecutive (memplan.cpp:15-29).  *shared_bytes = wpb*dim*4. */
+GNNA_API gnna_status gnna_build_mem_plan(gnna_ctx* ctx, const uint32_t* d_part2node,
+                                uint64_t num_groups, const gnna_params* p, uint8_t* d_slot,
+                                uint8_t* d_leader, uint64_t* shared_bytes);
+
+/* ------------------------------------------------------------- plans --- */
+/* Device-resident schedule for rows [row_begin, row_end) of a CSR graph:
+ * K1 units, K2 Algorithm-1 slots/leaders, run/carry layout.  The reference
+ * rebuilds this inside every aggregate_scheduled call (engine.cpp:213-221);
+ * here it is built once and reused.  The plan keeps pointers to d_row_ptr and
+ * d_col, which must outlive it.  Strategy NaiveAtomic/UnitSync flush every
+ * unit on its own, WarpShared per Algorithm-1 run. */
+GNNA_API gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                             uint32_t n, uint32_t row_begin, uint32_t row_end,
+                             const gnna_params* p, int strategy, gnna_plan** out);
+GNNA_API void gnna_plan_destroy(gnna_plan* plan);
+GNNA_API gnna_status gnna_plan_info(const gnna_plan* plan, uint64_t* num_groups, uint64_t* num_runs,
+                           uint64_t* num_split_nodes, uint64_t* num_carries);
+/* Device arrays of the plan (valid while the plan lives). */
+GNNA_API gnna_status gnna_plan_arrays(const gnna_plan* plan, const uint64_t** d_part_ptr,
+                             const uint32_t** d_part2node, const uint8_t** d_slot,
+                             const uint8_t** d_leader);
+
+/* ------------------------------------------------- aggregation (K3) --- */
+/* engine.hpp:71 aggregate_scheduled, values only: y[v] = sum_{u in N(v)} x[u]
+ * for the plan's rows, evaluated in the reference's summation tree (unit
+ * partials in CSR order -> Algorithm-1 run sums in unit order -> ordered
+ * cross-block combine).  GNNA_F64 is bitwise equal to the reference;
+ * GNNA_F32 follows the same tree in fp32.  x, y: n x dim row-major. */
+GNNA_API gnna_status gnna_aggregate(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
+                           const void* d_x, void* d_y);
+/* engine.hpp:30-53 + engine.cpp:242-289: the integer CostReport of
+ * aggregate_scheduled for this plan (K8).  cache_line == 0 disables the LRU
+ * replay (EngineOptions::cache = nullopt). */
+GNNA_API gnna_status gnna_cost_report(gnna_ctx* ctx, const gnna_plan* plan, int dim_mode,
+                             uint64_t line_bytes, uint64_t cache_capacity, uint64_t cache_line,
+                             gnna_cost* out);
+/* engine.hpp:77 simulate_cache over the plan's schedule. */
+GNNA_API gnna_status gnna_simulate_cache(gnna_ctx* ctx, const gnna_plan* plan, uint64_t cache_capacity,
+                                uint64_t cache_line, uint32_t dim, uint64_t* hits,
+                                uint64_t* accesses);
+
+/* engine.hpp:66 aggregate_oracle: y[v] = sum in CSR order (K4). */
+GNNA_API gnna_status gnna_aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
+                                const uint32_t* d_col, uint32_t n, uint32_t dim,
+                                const void* d_x, void* d_y);
+
+/* Host-buffer entry (what a drop-in aggregate_scheduled call does end to
+ * end): uploads CSR + x, plans, aggregates, downloads y (and the cost report
+ * when cost != NULL).  Host buffers may be pageable or pinned. */
+GNNA_API gnna_status gnna_aggregate_host(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr,
+                                const uint32_t* h_col, uint32_t n, const gnna_params* p,
+                                int strategy, int dim_mode, const void* h_x, void* h_y,
+                                uint64_t line_bytes, uint64_t cache_capacity,
+                                uint64_t cache_line, gnna_cost* cost);
+
+/* -------------------------------------------------------- GCN / GIN --- */
+/* engine.cpp:340-353: norm[v] = 1/sqrt(max(deg'(v),1)) (f64), deg' counts an
+ * implicit self loop when add_self_loops and v has none; d_self (u8, may be
+ * NULL) receives the implicit-self flags. */
+GNNA_API gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                          uint32_t n, int add_self_loops, double* d_norm, uint8_t* d_self);
+/* engine.cpp:338-369 normalized_aggregate, z = D^-1/2 (A [+I]) D^-1/2 x,
+ * F64 bitwise as the reference.  transpose != 0 applies the adjoint
+ * (out[u] += norm[v]norm[u] x[v]); it requires the transposed CSR
+ * (gnna_csr_transpose), which for a symmetric CSR is the CSR itself. */
+GNNA_API gnna_status gnna_normalized_aggregate(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
+                                      const uint32_t* d_col, uint32_t n, uint32_t dim,
+                                      const double* d_norm, const uint8_t* d_self,
+                                      const void* d_x, void* d_y);
+/* engine.cpp:315-331 matmul (K6): out = a (m x k) . w (k x n_out) [+ bias]
+ * [relu].  F64: k ascending, a==0 skipped, separate multiply and add —
+ * bitwise equal to the reference.  epilogue: 0 none, 1 bias+relu (GIN),
+ * 2 row scale by d_row_scale (f64 vector, used by the fp32 GCN fold). */
+GNNA_API gnna_status gnna_gemm(gnna_ctx* ctx, int dtype, const void* d_a, uint32_t m, uint32_t k,
+                      const void* d_w, uint32_t n_out, const void* d_bias, int epilogue,
+                      const double* d_row_scale, void* d_out);
+/* engine.hpp:93 gcn_layer / engine.hpp:108 gin_layer, forward (F64 bitwise). */
+GNNA_API gnna_status gnna_gcn_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
+                             const uint32_t* d_col, uint32_t n, const void* d_x,
+                             uint32_t in_dim, const void* d_w, uint32_t out_dim,
+                             int add_self_loops, void* d_y);
+GNNA_API gnna_status gnna_gin_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
+                             const uint32_t* d_col, uint32_t n, const void* d_x,
+                             uint32_t in_dim, double eps, const void* d_w, uint32_t out_dim,
+                             const void* d_b, void* d_y);
+/* Backward entry points (no reference function: SPEC.md:9 lists autograd as
+ * out of scope; added in the same style).  d_rt_ptr/d_rt_col is the
+ * transposed CSR (pass the CSR itself when it is symmetric, as to_csr(...,
+ * true) produces).  Gradients: GCN dx, dw; GIN dx, dw, db, deps (host). */
+GNNA_API gnna_status gnna_gcn_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
+                              const uint32_t* d_col, const uint64_t* d_rt_ptr,
+                              const uint32_t* d_rt_col, uint32_t n, const void* d_x,
+                              uint32_t in_dim, const void* d_w, uint32_t out_dim,
+                              int add_self_loops, const void* d_dy, void* d_dx, void* d_dw);
+GNNA_API gnna_status gnna_gin_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
+                              const uint32_t* d_col, const uint64_t* d_rt_ptr,
+                              const uint32_t* d_rt_col, uint32_t n, const void* d_x,
+                              uint32_t in_dim, double eps, const void* d_w, uint32_t out_dim,
+                              const void* d_b, const void* d_dy, void* d_dx, void* d_dw,
+                              void* d_db, double* deps);
+
+/* -------------------------------------------------- graph utilities --- */
+/* graph.cpp:76 to_csr on the GPU (symmetrize, sort rows, drop duplicates).
+ * Two-phase: call with d_col == NULL to get *nnz, then with a buffer of
+ * *nnz entries.  d_edges: E (src,dst) u32 pairs. */
+GNNA_API gnna_status gnna_to_csr(gnna_ctx* ctx, uint32_t n, const uint32_t* d_edges, uint64_t e,
+                        int symmetrize, uint64_t* d_row_ptr, uint32_t* d_col, uint64_t* nnz);
+/* CSR transpose (for the backward of non-symmetric graphs). */
+GNNA_API gnna_status gnna_csr_transpose(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                               uint32_t n, uint64_t* d_t_ptr, uint32_t* d_t_col);
+/* graph.cpp:122 aes (exact u64 span sum, then one divide). */
+GNNA_API gnna_status gnna_aes(gnna_ctx* ctx, const uint32_t* d_edges, uint64_t e, double* out);
+/* graph.cpp:106 degree_stats */
+GNNA_API gnna_status gnna_degree_stats(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n, double* avg,
+                              uint64_t* max_degree, double* stddev);
+
+/* -------------------------------------------------------- renumbering --- */
+/* renumber.cpp:31 detect_communities (exact greedy modularity merge order). */
+GNNA_API gnna_status gnna_detect_communities(gnna_ctx* ctx, const uint64_t* d_row_ptr,
+                                    const uint32_t* d_col, uint32_t n, uint32_t* d_com,
+                                    uint32_t* num_communities);
+/* renumber.cpp:106 modularity */
+GNNA_API gnna_status gnna_modularity(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                            uint32_t n, const uint32_t* d_com, uint32_t num_communities,
+                            double* q);
+/* renumber.cpp:128 build_mapping: order by (community, old id). */
+GNNA_API gnna_status gnna_build_mapping(gnna_ctx* ctx, const uint32_t* d_com, uint32_t n,
+                               uint32_t num_communities, uint32_t* d_old_to_new,
+                               uint32_t* d_new_to_old);
+/* renumber.cpp:148 mapping_from_vector (DOMAIN if not a permutation). */
+GNNA_API gnna_status gnna_mapping_from_vector(gnna_ctx* ctx, const uint32_t* d_vec, uint32_t n,
+                                     uint32_t* d_old_to_new, uint32_t* d_new_to_old);
+/* renumber.cpp:162 apply_mapping (CSR), output canonical (rows sorted). */
+GNNA_API gnna_status gnna_apply_mapping_csr(gnna_ctx* ctx, const uint64_t* d_row_ptr,
+                                   const uint32_t* d_col, uint32_t n,
+                                   const uint32_t* d_old_to_new, const uint32_t* d_new_to_old,
+                                   uint64_t* d_out_row_ptr, uint32_t* d_out_col);
+/* renumber.cpp:187 apply_mapping (EdgeList). */
+GNNA_API gnna_status gnna_apply_mapping_edges(gnna_ctx* ctx, const uint32_t* d_edges, uint64_t e,
+                                     uint32_t n, const uint32_t* d_old_to_new,
+                                     uint32_t* d_out_edges);
+
+/* ------------------------------------- performance evaluator (host) --- */
+/* decider.hpp:46-94, the reference's model with its defaults. */
+GNNA_API gnna_status gnna_model_inputs_from_graph(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
+                                         uint32_t dim, gnna_model_inputs* out);
+GNNA_API double gnna_alpha_from_degrees(double avg_degree, double stddev_degree);
+GNNA_API gnna_status gnna_select_dw(uint32_t dim, uint32_t tpw, uint32_t* out);
+GNNA_API gnna_status gnna_select_ngs(uint32_t dw, uint32_t tpb, const gnna_model_inputs* in,
+                            uint32_t* out);
+GNNA_API gnna_status gnna_dp_size(uint64_t smem_bytes, double avg_degree, double* out);
+GNNA_API gnna_status gnna_estimate_latency(const gnna_params* p, const gnna_model_inputs* in,
+                                  double* out);
+GNNA_API int gnna_candidate_feasible(const gnna_params* p, const gnna_model_inputs* in);
+GNNA_API int gnna_feasibility(const gnna_params* p, const gnna_model_inputs* in);
+GNNA_API gnna_status gnna_auto_params(const gnna_model_inputs* in, gnna_params* out);
+GNNA_API gnna_status gnna_search_params(const gnna_model_inputs* in, uint32_t iterations,
+                               uint32_t population, uint64_t seed, const uint32_t* gs_values,
+                               uint32_t n_gs, const uint32_t* dw_values, uint32_t n_dw,
+                               const uint32_t* tpb_values, uint32_t n_tpb, gnna_params* best,
+                               double* est_latency, int* feasible, double* trace,
+                               uint32_t* trace_len);
+/* B200 profile of the evaluator: 148 SMs, 227 KiB smem per block, runtime
+ * L2/HBM figures.  Fills `in` device fields from the live device. */
+GNNA_API gnna_status gnna_b200_profile(gnna_ctx* ctx, gnna_model_inputs* in);
+/* Measured-latency tuner: times gnna_aggregate (F32) on the live graph for
+ * every (ngs, dw, tpb) in the grid and returns the fastest (K3 sweep). */
+GNNA_API gnna_status gnna_tune_params(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                             uint32_t n, uint32_t dim, const uint32_t* gs_values, uint32_t n_gs,
+                             const uint32_t* dw_values, uint32_t n_dw,
+                             const uint32_t* tpb_values, uint32_t n_tpb, gnna_params* best,
+                             float* best_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNA_H */

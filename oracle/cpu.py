@@ -78,18 +78,18 @@ class Oracle:
         if not os.path.exists(self.path):
             raise FileNotFoundError(f"{self.path} not built (run __graft_entry__.build())")
         self.lib = C.CDLL(self.path)
-        self.lib[f"{kind}_last_error"].restype = C.c_char_p
+        self._err = getattr(self.lib, f"{kind}_last_error")
+        self._err.restype = C.c_char_p
 
     def _fn(self, name):
-        f = self.lib[f"{self.kind}_{name}"]
-        return f
+        return getattr(self.lib, f"{self.kind}_{name}")
 
     def _call(self, name, *args):
         f = self._fn(name)
         f.restype = C.c_int
         rc = f(*args)
         if rc != 0:
-            msg = self.lib[f"{self.kind}_last_error"]().decode()
+            msg = self._err().decode()
             raise OracleError(rc, msg)
 
     # ------------------------------------------------------------- graph

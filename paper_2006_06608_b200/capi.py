@@ -1,0 +1,273 @@
+"""ctypes binding of libgnna.so (include/gnna.h) for Python callers.
+
+Device memory, streams and collectives come from PyTorch (plumbing only); all
+compute happens in libgnna.so's sm_100a kernels.  There is no fallback: if the
+library is missing or the device is not a B200 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgnna.so")
+
+OK, ERR_DOMAIN, ERR_INTERNAL, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
+NAIVE_ATOMIC, UNIT_SYNC, WARP_SHARED = 0, 1, 2
+DIM_SEQUENTIAL, DIM_CYCLIC = 0, 1
+F32, F64 = 0, 1
+
+
+class GnnaError(RuntimeError):
+    KIND = {ERR_DOMAIN: "DomainError", ERR_INTERNAL: "InternalError", ERR_CUDA: "CudaError",
+            ERR_OOM: "OutOfMemory"}
+
+    def __init__(self, code, msg):
+        super().__init__(f"{self.KIND.get(code, code)}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class DomainError(GnnaError):
+    pass
+
+
+class Params(C.Structure):
+    """schedule.hpp:14-27 KernelParams."""
+    _fields_ = [("ngs", C.c_uint32), ("dw", C.c_uint32), ("tpb", C.c_uint32), ("tpw", C.c_uint32),
+                ("dim", C.c_uint32)]
+
+    @classmethod
+    def make(cls, ngs=16, dw=32, tpb=128, dim=16, tpw=32):
+        return cls(ngs, dw, tpb, tpw, dim)
+
+    def tolist(self):
+        return [self.ngs, self.dw, self.tpb, self.tpw, self.dim]
+
+
+class Cost(C.Structure):
+    """engine.hpp:30-53 CostReport."""
+    _fields_ = [(k, C.c_uint64) for k in ("atomic_ops", "global_reads", "global_writes",
+                                          "global_transactions", "shared_bytes_per_block",
+                                          "cache_hits", "cache_accesses")]
+
+    def tolist(self):
+        return [getattr(self, k) for k, _ in self._fields_]
+
+
+class ModelInputs(C.Structure):
+    """decider.hpp:12-26 ModelInputs."""
+    _fields_ = [("num_nodes", C.c_uint64), ("num_edges", C.c_uint64), ("dim", C.c_uint32),
+                ("max_tpb", C.c_uint32), ("avg_degree", C.c_double),
+                ("stddev_degree", C.c_double), ("smem_per_block", C.c_uint64),
+                ("capability", C.c_uint64), ("alpha", C.c_double)]
+
+    @classmethod
+    def make(cls, num_nodes=0, num_edges=0, dim=16, avg_degree=0.0, stddev_degree=0.0,
+             max_tpb=1024, smem_per_block=96 * 1024, capability=4096, alpha=0.15):
+        return cls(num_nodes, num_edges, dim, max_tpb, avg_degree, stddev_degree, smem_per_block,
+                   capability, alpha)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+        _lib = C.CDLL(LIB_PATH)
+        _lib.gnna_last_error.restype = C.c_char_p
+        _lib.gnna_version.restype = C.c_char_p
+        _lib.gnna_launch_count.restype = C.c_uint64
+        _lib.gnna_get_stream.restype = C.c_void_p
+        _lib.gnna_alpha_from_degrees.restype = C.c_double
+        _lib.gnna_alpha_from_degrees.argtypes = [C.c_double, C.c_double]
+    return _lib
+
+
+def _ptr(t):
+    if t is None:
+        return C.c_void_p(0)
+    if isinstance(t, np.ndarray):
+        return C.c_void_p(t.ctypes.data)
+    return C.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.float64:
+        return F64
+    raise TypeError(f"unsupported feature dtype {t.dtype}")
+
+
+class Context:
+    """One gnna_ctx bound to a CUDA device; kernels run on torch's current
+    stream (captured at construction, or call set_stream)."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        self.torch = torch
+        self.L = lib()
+        self.device = device
+        h = C.c_void_p()
+        rc = self.L.gnna_create(C.c_int(device), C.byref(h))
+        if rc:
+            raise GnnaError(rc, "gnna_create failed (needs a B200 / sm_100 device)")
+        self.h = h
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.set_stream(stream)
+
+    def set_stream(self, stream):
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._check(self.L.gnna_set_stream(self.h, C.c_void_p(handle)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.gnna_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != OK:
+            msg = self.L.gnna_last_error(self.h).decode()
+            if rc == ERR_DOMAIN:
+                raise DomainError(rc, msg)
+            raise GnnaError(rc, msg)
+
+    @property
+    def launches(self):
+        return int(self.L.gnna_launch_count(self.h))
+
+    def synchronize(self):
+        self._check(self.L.gnna_synchronize(self.h))
+
+    def _empty(self, n, dtype):
+        return self.torch.empty(n, dtype=dtype, device=f"cuda:{self.device}")
+
+    # ------------------------------------------------------- preprocessing
+    def validate_params(self, p: Params):
+        self._check(self.L.gnna_validate_params(self.h, C.byref(p)))
+
+    def count_groups(self, row_ptr, ngs):
+        g = C.c_uint64()
+        self._check(self.L.gnna_count_groups(self.h, _ptr(row_ptr), C.c_uint32(row_ptr.numel() - 1),
+                                             C.c_uint32(ngs), C.byref(g)))
+        return g.value
+
+    def partition_neighbors(self, row_ptr, ngs):
+        """schedule.cpp:16 -> (part_ptr[G+1] int64, part2node[G] int32) device tensors."""
+        torch = self.torch
+        G = self.count_groups(row_ptr, ngs)
+        pp = self._empty(G + 1, torch.int64)
+        p2n = self._empty(max(G, 1), torch.int32)
+        self._check(self.L.gnna_partition_neighbors(self.h, _ptr(row_ptr), C.c_uint32(row_ptr.numel() - 1),
+                                                    C.c_uint32(ngs), _ptr(pp), _ptr(p2n)))
+        return pp, p2n[:G]
+
+    def build_mem_plan(self, part2node, p: Params):
+        """memplan.cpp:9 -> (slot u8[G], leader u8[G], shared_bytes)."""
+        torch = self.torch
+        G = part2node.numel()
+        slot = self._empty(max(G, 1), torch.uint8)
+        lead = self._empty(max(G, 1), torch.uint8)
+        sb = C.c_uint64()
+        self._check(self.L.gnna_build_mem_plan(self.h, _ptr(part2node), C.c_uint64(G), C.byref(p),
+                                               _ptr(slot), _ptr(lead), C.byref(sb)))
+        return slot[:G], lead[:G], sb.value
+
+    def plan(self, row_ptr, col, p: Params, strategy=WARP_SHARED, rows=None):
+        return Plan(self, row_ptr, col, p, strategy, rows)
+
+    # --------------------------------------------------------- aggregation
+    def aggregate_rows(self, row_ptr, col, x, out=None):
+        n = row_ptr.numel() - 1
+        if out is None:
+            out = self.torch.empty_like(x)
+        self._check(self.L.gnna_aggregate_rows(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col),
+                                               C.c_uint32(n), C.c_uint32(x.shape[1]), _ptr(x), _ptr(out)))
+        return out
+
+    def aggregate_host(self, row_ptr, col, x, p: Params, strategy=WARP_SHARED, dim_mode=DIM_CYCLIC,
+                       out=None, line=128, cache=None, want_cost=True):
+        """gnna_aggregate_host: host (numpy / pinned torch CPU) buffers in and out."""
+        n = len(row_ptr) - 1
+        if out is None:
+            out = np.empty_like(x)
+        dt = F32 if x.dtype in (np.float32,) or str(x.dtype) == "torch.float32" else F64
+        cost = Cost()
+        cap, cl = cache if cache else (0, 0)
+        self._check(self.L.gnna_aggregate_host(self.h, C.c_int(dt), _ptr(row_ptr), _ptr(col), C.c_uint32(n),
+                                               C.byref(p), C.c_int(strategy), C.c_int(dim_mode), _ptr(x),
+                                               _ptr(out), C.c_uint64(line), C.c_uint64(cap), C.c_uint64(cl),
+                                               C.byref(cost) if want_cost else None))
+        return out, cost
+
+    # ------------------------------------------------------------- decider
+    def auto_params(self, inputs: ModelInputs) -> Params:
+        p = Params()
+        rc = self.L.gnna_auto_params(C.byref(inputs), C.byref(p))
+        if rc:
+            raise DomainError(rc, "auto_params")
+        return p
+
+
+class Plan:
+    def __init__(self, ctx: Context, row_ptr, col, p: Params, strategy=WARP_SHARED, rows=None):
+        self.ctx = ctx
+        self.row_ptr, self.col = row_ptr, col  # keep alive
+        self.params = Params(*p.tolist())
+        self.strategy = strategy
+        n = row_ptr.numel() - 1
+        r0, r1 = rows if rows is not None else (0, n)
+        self.n, self.rows = n, (r0, r1)
+        h = C.c_void_p()
+        ctx._check(ctx.L.gnna_plan_create(ctx.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), C.c_uint32(r0),
+                                          C.c_uint32(r1), C.byref(self.params), C.c_int(strategy),
+                                          C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ctx.L.gnna_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self):
+        g, r, s, c = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self.ctx._check(self.ctx.L.gnna_plan_info(self.h, C.byref(g), C.byref(r), C.byref(s), C.byref(c)))
+        return {"groups": g.value, "runs": r.value, "split_nodes": s.value, "carries": c.value}
+
+    def aggregate(self, x, out=None, dim_mode=DIM_CYCLIC):
+        if out is None:
+            out = self.ctx.torch.zeros_like(x)
+        self.ctx._check(self.ctx.L.gnna_aggregate(self.ctx.h, self.h, C.c_int(_dtype_code(x)),
+                                                  C.c_int(dim_mode), _ptr(x), _ptr(out)))
+        return out
+
+    def cost(self, dim_mode=DIM_CYCLIC, line=128, cache=None):
+        c = Cost()
+        cap, cl = cache if cache else (0, 0)
+        self.ctx._check(self.ctx.L.gnna_cost_report(self.ctx.h, self.h, C.c_int(dim_mode), C.c_uint64(line),
+                                                    C.c_uint64(cap), C.c_uint64(cl), C.byref(c)))
+        return c
+
+    def simulate_cache(self, cache, dim):
+        h, a = C.c_uint64(), C.c_uint64()
+        self.ctx._check(self.ctx.L.gnna_simulate_cache(self.ctx.h, self.h, C.c_uint64(cache[0]),
+                                                       C.c_uint64(cache[1]), C.c_uint32(dim), C.byref(h),
+                                                       C.byref(a)))
+        return h.value, a.value

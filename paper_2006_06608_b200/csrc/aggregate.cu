@@ -1,0 +1,522 @@
+// K3 / K3b / K4: neighbor aggregation for sm_100a.
+//
+// K3 (scheduled, engine.cpp:200-311): a team of TEAM lanes owns one workload
+// unit (neighbor group).  Lanes split the row into 16-byte vectors (float4 /
+// double2; the north star's "dimension workers"): lane t owns vector chunks
+// t, t+TEAM, ... (Cyclic) or a contiguous block (Sequential).  A CTA holds
+// whole schedule blocks (wpb units, Algorithm 1), so every run is CTA-local:
+//   - a unit that is a whole run of a node living in one block stores its
+//     partial straight to HBM (the common case once ngs >= degree);
+//   - otherwise partials go to shared memory and the run's leader team sums
+//     them in unit order (= the reference's slot accumulation) and flushes;
+//   - a run of a node spanning several blocks is written to a carry slot and
+//     K3b adds the node's carries in block order.
+// The summation tree is the reference's: per unit, sequential over CSR
+// order from 0; per run, sequential over units from 0; per node, sequential
+// over blocks from 0.  In fp64 this makes the result bitwise equal to
+// aggregate_scheduled; in fp32 it is the same tree in fp32.  No float
+// atomics anywhere, so results are run-to-run deterministic.
+//
+// K4 (rows): one team per CSR row, CSR order (aggregate_oracle,
+// engine.cpp:149-160), with exact fp64 variants of normalized_aggregate
+// (engine.cpp:355-367) and the GIN self term (engine.cpp:394-400).
+#include <algorithm>
+
+#include "gnna_common.cuh"
+
+namespace {
+
+using gnna::DevBuf;
+
+template <class T, int VEC>
+struct alignas(sizeof(T) * VEC) Vec {
+    T a[VEC];
+};
+
+template <class T, int VEC>
+__device__ __forceinline__ Vec<T, VEC> ldv(const T* p) {
+    Vec<T, VEC> r;
+    if constexpr (sizeof(T) * VEC == 16 && sizeof(T) == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        r.a[0] = t.x; r.a[1] = t.y; r.a[2] = t.z; r.a[3] = t.w;
+    } else if constexpr (sizeof(T) * VEC == 16 && sizeof(T) == 8) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        r.a[0] = t.x; r.a[1] = t.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) r.a[i] = __ldg(p + i);
+    }
+    return r;
+}
+
+template <class T, int VEC>
+__device__ __forceinline__ void stv(T* p, const Vec<T, VEC>& v) {
+    if constexpr (sizeof(T) * VEC == 16 && sizeof(T) == 4) {
+        __stcs(reinterpret_cast<float4*>(p), make_float4(v.a[0], v.a[1], v.a[2], v.a[3]));
+    } else if constexpr (sizeof(T) * VEC == 16 && sizeof(T) == 8) {
+        __stcs(reinterpret_cast<double2*>(p), make_double2(v.a[0], v.a[1]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) p[i] = v.a[i];
+    }
+}
+
+template <class T, int VEC>
+__device__ __forceinline__ void vzero(Vec<T, VEC>& v) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) v.a[i] = T(0);
+}
+
+// acc += v, one IEEE add per element (never contracted: no multiply).
+template <class T, int VEC>
+__device__ __forceinline__ void vadd(Vec<T, VEC>& acc, const Vec<T, VEC>& v) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc.a[i] = acc.a[i] + v.a[i];
+}
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+// acc += c * v with a separately rounded product (the reference's
+// `out[d] += c * in[d]` compiled without FMA contraction).
+template <class T, int VEC>
+__device__ __forceinline__ void vaxpy_rn(Vec<T, VEC>& acc, T c, const Vec<T, VEC>& v) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc.a[i] = add_rn(acc.a[i], mul_rn(c, v.a[i]));
+}
+
+enum : uint32_t { EPI_SCALE = 1, EPI_SELF = 2, EPI_RELU = 4 };
+
+struct AggArgs {
+    // schedule
+    const uint64_t* part_ptr;
+    const uint32_t* part2node;
+    const uint8_t* uflags;
+    const uint32_t* cidx;
+    uint64_t units;    // K3: plan units; K4: rows
+    uint32_t upc;      // units per CTA
+    uint32_t r0;       // K4: first row
+    const uint64_t* row_ptr;
+    const uint32_t* col;
+    const void* x;
+    void* y;
+    void* carry;
+    uint32_t dim, nvec, kpl;
+    int seq;
+    // epilogue (final writes only)
+    uint32_t epi;
+    const float* scale;   // EPI_SCALE: per-row multiplier (fp32 GCN fold)
+    double alpha;         // EPI_SELF:  y += alpha * x[v]
+    // K4 exact modes
+    const double* norm;
+    const uint8_t* self;
+};
+
+template <class T, int VEC, int TEAM, int KMAX>
+struct Lanes {
+    uint32_t off[KMAX];
+    bool ok[KMAX];
+    __device__ __forceinline__ void init(const AggArgs& a, uint32_t lane, uint32_t k0) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const uint32_t kk = k0 + k;
+            const uint32_t c = a.seq ? lane * a.kpl + kk : lane + kk * TEAM;
+            ok[k] = kk < a.kpl && c < a.nvec;
+            off[k] = c * VEC;
+        }
+    }
+};
+
+template <class T, int VEC>
+__device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32_t off, Vec<T, VEC> val) {
+    T* y = static_cast<T*>(a.y) + (size_t)v * a.dim + off;
+    if (a.epi) {
+        if (a.epi & EPI_SELF) {
+            const Vec<T, VEC> xv = ldv<T, VEC>(static_cast<const T*>(a.x) + (size_t)v * a.dim + off);
+            vaxpy_rn(val, T(a.alpha), xv);
+        }
+        if (a.epi & EPI_SCALE) {
+            const T s = T(a.scale[v]);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) val.a[i] = s * val.a[i];
+        }
+        if (a.epi & EPI_RELU) {
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) val.a[i] = val.a[i] > T(0) ? val.a[i] : T(0);
+        }
+    }
+    stv<T, VEC>(y, val);
+}
+
+// Sequential gather over [b, e) into acc (CSR order; UNR loads in flight
+// per lane, added in edge order).
+template <class T, int VEC, int KMAX>
+__device__ __forceinline__ void gather(const AggArgs& a, uint64_t b, uint64_t e, const uint32_t (&off)[KMAX],
+                                       const bool (&ok)[KMAX], Vec<T, VEC> (&acc)[KMAX]) {
+    constexpr int UNR = 8 / KMAX;
+    const T* __restrict__ x = static_cast<const T*>(a.x);
+    const uint32_t* __restrict__ col = a.col;
+    uint64_t p = b;
+    for (; p + UNR <= e; p += UNR) {
+        uint32_t idx[UNR];
+#pragma unroll
+        for (int j = 0; j < UNR; ++j) idx[j] = __ldg(col + p + j);
+        Vec<T, VEC> val[UNR][KMAX];
+#pragma unroll
+        for (int j = 0; j < UNR; ++j)
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (ok[k]) val[j][k] = ldv<T, VEC>(x + (size_t)idx[j] * a.dim + off[k]);
+#pragma unroll
+        for (int j = 0; j < UNR; ++j)
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (ok[k]) vadd(acc[k], val[j][k]);
+    }
+    for (; p < e; ++p) {
+        const uint32_t idx = __ldg(col + p);
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (ok[k]) vadd(acc[k], ldv<T, VEC>(x + (size_t)idx * a.dim + off[k]));
+    }
+}
+
+// ----------------------------------------------------------------- K3 ---
+template <class T, int VEC, int TEAM, int KMAX>
+__global__ void __launch_bounds__(256) k3_aggregate(AggArgs a) {
+    using VT = Vec<T, VEC>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    VT* sm = reinterpret_cast<VT*>(smem_raw);  // [upc][KMAX][TEAM]
+    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
+    const uint64_t u = (uint64_t)blockIdx.x * a.upc + tu;
+    const bool active = tu < a.upc && u < a.units;
+    uint64_t b = 0, e = 0;
+    uint32_t v = 0;
+    uint8_t f = 0;
+    if (active) {
+        b = __ldg(a.part_ptr + u);
+        e = __ldg(a.part_ptr + u + 1);
+        v = __ldg(a.part2node + u);
+        f = __ldg(a.uflags + u);
+    }
+    const bool direct = (f & (UF_LEADER | UF_RUN_END)) == (UF_LEADER | UF_RUN_END) && !(f & UF_SPLIT);
+    const bool staged = active && !direct;
+    const bool need_smem = __syncthreads_or(staged);
+    for (uint32_t k0 = 0; k0 < a.kpl; k0 += KMAX) {
+        Lanes<T, VEC, TEAM, KMAX> L;
+        L.init(a, lane, k0);
+        VT acc[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) vzero(acc[k]);
+        if (active) gather<T, VEC, KMAX>(a, b, e, L.off, L.ok, acc);
+        if (active && direct) {
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (L.ok[k]) store_final<T, VEC>(a, v, L.off[k], acc[k]);
+        }
+        if (need_smem) {
+            if (staged) {
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k) sm[(tu * KMAX + k) * TEAM + lane] = acc[k];
+            }
+            __syncthreads();
+            if (staged && (f & UF_LEADER)) {
+                VT r[KMAX];
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k) vzero(r[k]);
+                uint32_t t2 = tu;
+                uint8_t f2 = f;
+                for (;;) {
+#pragma unroll
+                    for (int k = 0; k < KMAX; ++k) vadd(r[k], sm[(t2 * KMAX + k) * TEAM + lane]);
+                    if (f2 & UF_RUN_END) break;
+                    ++t2;
+                    f2 = __ldg(a.uflags + u + (t2 - tu));
+                }
+                if (f & UF_SPLIT) {
+                    T* cy = static_cast<T*>(a.carry) + (size_t)__ldg(a.cidx + u) * a.dim;
+#pragma unroll
+                    for (int k = 0; k < KMAX; ++k)
+                        if (L.ok[k]) stv<T, VEC>(cy + L.off[k], r[k]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < KMAX; ++k)
+                        if (L.ok[k]) store_final<T, VEC>(a, v, L.off[k], r[k]);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// K3b: split nodes add their carried run sums in block order (from 0);
+// empty rows get the epilogue of a zero sum.
+template <class T, int VEC, int TEAM>
+__global__ void __launch_bounds__(256) k3b_fixup(AggArgs a, const uint32_t* __restrict__ nodes,
+                                                 const uint32_t* __restrict__ first,
+                                                 const uint32_t* __restrict__ count, uint64_t nsplit,
+                                                 uint64_t nfix) {
+    using VT = Vec<T, VEC>;
+    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
+    const uint64_t i = (uint64_t)blockIdx.x * (256 / TEAM) + tu;
+    if (i >= nfix) return;
+    const uint32_t v = nodes[i];
+    for (uint32_t c = lane; c < a.nvec; c += TEAM) {
+        VT acc;
+        vzero(acc);
+        if (i < nsplit) {
+            const T* cy = static_cast<const T*>(a.carry) + (size_t)first[i] * a.dim + c * VEC;
+            const uint32_t cnt = count[i];
+            for (uint32_t j = 0; j < cnt; ++j) vadd(acc, ldv<T, VEC>(cy + (size_t)j * a.dim));
+        }
+        store_final<T, VEC>(a, v, c * VEC, acc);
+    }
+}
+
+// ----------------------------------------------------------------- K4 ---
+// MODE 0: plain CSR-order sum.  MODE 1: exact normalized_aggregate (per-edge
+// c = norm[v]*norm[u], separately rounded c*x, implicit self loop last).
+// MODE 2: exact GIN input (CSR-order sum, then + alpha*x[v]).
+template <class T, int VEC, int TEAM, int KMAX, int MODE>
+__global__ void __launch_bounds__(256) k4_rows(AggArgs a) {
+    using VT = Vec<T, VEC>;
+    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
+    const uint64_t i = (uint64_t)blockIdx.x * (256 / TEAM) + tu;
+    if (i >= a.units) return;
+    const uint32_t v = a.r0 + (uint32_t)i;
+    const uint64_t b = __ldg(a.row_ptr + v), e = __ldg(a.row_ptr + v + 1);
+    const T* __restrict__ x = static_cast<const T*>(a.x);
+    for (uint32_t k0 = 0; k0 < a.kpl; k0 += KMAX) {
+        Lanes<T, VEC, TEAM, KMAX> L;
+        L.init(a, lane, k0);
+        VT acc[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) vzero(acc[k]);
+        if constexpr (MODE == 1) {
+            const double nv = a.norm[v];
+            for (uint64_t p = b; p < e; ++p) {
+                const uint32_t uu = __ldg(a.col + p);
+                const T c = T(__dmul_rn(nv, a.norm[uu]));
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (L.ok[k]) vaxpy_rn(acc[k], c, ldv<T, VEC>(x + (size_t)uu * a.dim + L.off[k]));
+            }
+            if (a.self && a.self[v]) {
+                const T c = T(__dmul_rn(nv, nv));
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (L.ok[k]) vaxpy_rn(acc[k], c, ldv<T, VEC>(x + (size_t)v * a.dim + L.off[k]));
+            }
+        } else {
+            gather<T, VEC, KMAX>(a, b, e, L.off, L.ok, acc);
+            if constexpr (MODE == 2) {
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (L.ok[k]) vaxpy_rn(acc[k], T(a.alpha), ldv<T, VEC>(x + (size_t)v * a.dim + L.off[k]));
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (L.ok[k]) store_final<T, VEC>(a, v, L.off[k], acc[k]);
+    }
+}
+
+// ----------------------------------------------------------- dispatch ---
+uint32_t pow2ceil(uint32_t v) {
+    uint32_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+uint32_t pow2floor(uint32_t v) {
+    uint32_t p = 1;
+    while (p * 2 <= v) p <<= 1;
+    return p;
+}
+
+struct Shape {
+    int vec;
+    uint32_t team, kpl, kmax;
+};
+
+Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const void* x, const void* y) {
+    Shape s;
+    const int full = 16 / elem;
+    const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+    s.vec = (dim % full == 0 && aligned) ? full : 1;
+    const uint32_t nvec = dim / s.vec;
+    // dw counts scalar dimension workers (schedule.hpp:16); with 16-byte
+    // lanes one vector lane stands for `vec` of them.
+    uint32_t t = pow2ceil((dw + s.vec - 1) / s.vec);
+    t = std::min<uint32_t>(t, pow2ceil(nvec));
+    t = std::min<uint32_t>(t, team_cap);
+    t = std::max<uint32_t>(t, 1);
+    s.team = std::min<uint32_t>(t, 32);
+    s.kpl = (nvec + s.team - 1) / s.team;
+    s.kmax = s.kpl <= 1 ? 1 : 4;
+    return s;
+}
+
+template <class T, int VEC, int TEAM>
+void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, const gnna_plan* plan) {
+    const size_t smem = (size_t)a.upc * kmax * TEAM * sizeof(Vec<T, VEC>);
+    if (grid) {
+        if (kmax == 1)
+            k3_aggregate<T, VEC, TEAM, 1><<<(unsigned)grid, a.upc * TEAM, smem, ctx->stream>>>(a);
+        else
+            k3_aggregate<T, VEC, TEAM, 4><<<(unsigned)grid, a.upc * TEAM, smem, ctx->stream>>>(a);
+        gnna::launched(ctx, "k3_aggregate");
+    }
+    const uint64_t nfix = plan->nsplit + plan->nempty;
+    if (nfix) {
+        k3b_fixup<T, VEC, TEAM><<<(unsigned)((nfix + 256 / TEAM - 1) / (256 / TEAM)), 256, 0, ctx->stream>>>(
+            a, plan->fix_nodes.get(), plan->fix_first.get(), plan->fix_count.get(), plan->nsplit, nfix);
+        gnna::launched(ctx, "k3b_fixup");
+    }
+}
+
+template <class T, int VEC>
+void launch_k3(gnna_ctx* ctx, AggArgs& a, const Shape& s, uint64_t grid, const gnna_plan* plan) {
+    switch (s.team) {
+        case 1: launch_k3_team<T, VEC, 1>(ctx, a, s.kmax, grid, plan); break;
+        case 2: launch_k3_team<T, VEC, 2>(ctx, a, s.kmax, grid, plan); break;
+        case 4: launch_k3_team<T, VEC, 4>(ctx, a, s.kmax, grid, plan); break;
+        case 8: launch_k3_team<T, VEC, 8>(ctx, a, s.kmax, grid, plan); break;
+        case 16: launch_k3_team<T, VEC, 16>(ctx, a, s.kmax, grid, plan); break;
+        default: launch_k3_team<T, VEC, 32>(ctx, a, s.kmax, grid, plan); break;
+    }
+}
+
+template <class T, int VEC, int TEAM, int MODE>
+void launch_k4_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax) {
+    const unsigned grid = (unsigned)((a.units + 256 / TEAM - 1) / (256 / TEAM));
+    if (kmax == 1)
+        k4_rows<T, VEC, TEAM, 1, MODE><<<grid, 256, 0, ctx->stream>>>(a);
+    else
+        k4_rows<T, VEC, TEAM, 4, MODE><<<grid, 256, 0, ctx->stream>>>(a);
+    gnna::launched(ctx, "k4_rows");
+}
+
+template <class T, int VEC, int MODE>
+void launch_k4(gnna_ctx* ctx, AggArgs& a, const Shape& s) {
+    switch (s.team) {
+        case 1: launch_k4_team<T, VEC, 1, MODE>(ctx, a, s.kmax); break;
+        case 2: launch_k4_team<T, VEC, 2, MODE>(ctx, a, s.kmax); break;
+        case 4: launch_k4_team<T, VEC, 4, MODE>(ctx, a, s.kmax); break;
+        case 8: launch_k4_team<T, VEC, 8, MODE>(ctx, a, s.kmax); break;
+        case 16: launch_k4_team<T, VEC, 16, MODE>(ctx, a, s.kmax); break;
+        default: launch_k4_team<T, VEC, 32, MODE>(ctx, a, s.kmax); break;
+    }
+}
+
+}  // namespace
+
+namespace gnna {
+
+// Scheduled aggregation over a plan (K3 + K3b).  epi/scale/alpha: epilogue.
+void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                    uint32_t epi, const float* scale, double alpha) {
+    if (!plan) raise(GNNA_ERR_DOMAIN, "null plan");
+    if (dtype != GNNA_F32 && dtype != GNNA_F64) raise(GNNA_ERR_DOMAIN, "unknown dtype");
+    const uint32_t dim = plan->params.dim;
+    const int elem = dtype == GNNA_F32 ? 4 : 8;
+    const uint32_t wpb = plan->wpb;
+    const Shape s = choose_shape(elem, dim, plan->params.dw, pow2floor(256 / wpb), x, y);
+    AggArgs a{};
+    a.part_ptr = plan->part_ptr.get();
+    a.part2node = plan->part2node.get();
+    a.uflags = plan->uflags.get();
+    a.cidx = plan->cidx.get();
+    a.units = plan->G;
+    a.upc = ((256 / s.team) / wpb) * wpb;
+    a.row_ptr = plan->row_ptr;
+    a.col = plan->col;
+    a.x = x;
+    a.y = y;
+    a.carry = plan->carry.get();
+    a.dim = dim;
+    a.nvec = dim / s.vec;
+    a.kpl = s.kpl;
+    a.seq = dim_mode == GNNA_DIM_SEQUENTIAL;
+    a.epi = epi;
+    a.scale = scale;
+    a.alpha = alpha;
+    if (plan->G == 0 && plan->nempty == 0) return;
+    const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;
+    if (grid > 0x7fffffffull) raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
+    if (dtype == GNNA_F32) {
+        if (s.vec == 4) launch_k3<float, 4>(ctx, a, s, grid, plan);
+        else launch_k3<float, 1>(ctx, a, s, grid, plan);
+    } else {
+        if (s.vec == 2) launch_k3<double, 2>(ctx, a, s, grid, plan);
+        else launch_k3<double, 1>(ctx, a, s, grid, plan);
+    }
+}
+
+// Row-order aggregation (K4).  mode 0 sum, 1 exact normalized, 2 exact GIN input.
+void aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* row_ptr, const uint32_t* col, uint32_t r0,
+                    uint32_t rows, uint32_t dim, const void* x, void* y, int mode, const double* norm,
+                    const uint8_t* self, double alpha, uint32_t epi, const float* scale) {
+    if (dtype != GNNA_F32 && dtype != GNNA_F64) raise(GNNA_ERR_DOMAIN, "unknown dtype");
+    if (rows == 0 || dim == 0) return;
+    const int elem = dtype == GNNA_F32 ? 4 : 8;
+    const Shape s = choose_shape(elem, dim, 32 * 4, 32, x, y);
+    AggArgs a{};
+    a.units = rows;
+    a.r0 = r0;
+    a.row_ptr = row_ptr;
+    a.col = col;
+    a.x = x;
+    a.y = y;
+    a.dim = dim;
+    a.nvec = dim / s.vec;
+    a.kpl = s.kpl;
+    a.seq = 0;
+    a.epi = epi;
+    a.scale = scale;
+    a.alpha = alpha;
+    a.norm = norm;
+    a.self = self;
+    if (dtype == GNNA_F32) {
+        if (mode == 1) {
+            if (s.vec == 4) launch_k4<float, 4, 1>(ctx, a, s); else launch_k4<float, 1, 1>(ctx, a, s);
+        } else if (mode == 2) {
+            if (s.vec == 4) launch_k4<float, 4, 2>(ctx, a, s); else launch_k4<float, 1, 2>(ctx, a, s);
+        } else {
+            if (s.vec == 4) launch_k4<float, 4, 0>(ctx, a, s); else launch_k4<float, 1, 0>(ctx, a, s);
+        }
+    } else {
+        if (mode == 1) {
+            if (s.vec == 2) launch_k4<double, 2, 1>(ctx, a, s); else launch_k4<double, 1, 1>(ctx, a, s);
+        } else if (mode == 2) {
+            if (s.vec == 2) launch_k4<double, 2, 2>(ctx, a, s); else launch_k4<double, 1, 2>(ctx, a, s);
+        } else {
+            if (s.vec == 2) launch_k4<double, 2, 0>(ctx, a, s); else launch_k4<double, 1, 0>(ctx, a, s);
+        }
+    }
+}
+
+}  // namespace gnna
+
+extern "C" {
+
+gnna_status gnna_aggregate(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* d_x,
+                           void* d_y) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        gnna::aggregate_plan(ctx, plan, dtype, dim_mode, d_x, d_y, 0, nullptr, 0.0);
+    });
+}
+
+gnna_status gnna_aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                                uint32_t n, uint32_t dim, const void* d_x, void* d_y) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, dim, d_x, d_y, 0, nullptr, nullptr, 0.0, 0,
+                             nullptr);
+    });
+}
+
+}  // extern "C"

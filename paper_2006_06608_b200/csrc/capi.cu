@@ -1,0 +1,96 @@
+// Context lifecycle and the host-buffer end-to-end entry of include/gnna.h.
+#include <cstring>
+
+#include "gnna_common.cuh"
+
+namespace gnna {
+void validate_params(const gnna_params* p);
+void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                    uint32_t epi, const float* scale, double alpha);
+void cost_report(gnna_ctx* ctx, const gnna_plan* plan, int dim_mode, uint64_t line, uint64_t cache_cap,
+                 uint64_t cache_line, gnna_cost* out);
+}  // namespace gnna
+
+extern "C" {
+
+const char* gnna_version(void) { return "gnna-b200 0.1 (sm_100a)"; }
+
+gnna_status gnna_create(int device, gnna_ctx** out) {
+    return gnna::guard(nullptr, [&] {
+        if (!out) gnna::raise(GNNA_ERR_DOMAIN, "null output pointer");
+        int count = 0;
+        GNNA_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) gnna::raise(GNNA_ERR_CUDA, "no such CUDA device");
+        int major = 0, minor = 0;
+        GNNA_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        GNNA_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device));
+        if (major != 10 || minor != 0)
+            gnna::raise(GNNA_ERR_CUDA, "libgnna is built for sm_100a (B200); device is sm_" +
+                                           std::to_string(major) + std::to_string(minor));
+        GNNA_CUDA(cudaSetDevice(device));
+        auto ctx = new gnna_ctx();
+        ctx->device = device;
+        cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+        cudaDeviceGetAttribute(&ctx->l2_bytes, cudaDevAttrL2CacheSize, device);
+        cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+        *out = ctx;
+    });
+}
+
+void gnna_destroy(gnna_ctx* ctx) { delete ctx; }
+
+gnna_status gnna_set_stream(gnna_ctx* ctx, void* stream) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+void* gnna_get_stream(const gnna_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+gnna_status gnna_synchronize(gnna_ctx* ctx) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        GNNA_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+const char* gnna_last_error(const gnna_ctx* ctx) { return ctx ? ctx->err.c_str() : "null gnna_ctx"; }
+
+uint64_t gnna_launch_count(const gnna_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+gnna_status gnna_aggregate_host(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr, const uint32_t* h_col,
+                                uint32_t n, const gnna_params* p, int strategy, int dim_mode, const void* h_x,
+                                void* h_y, uint64_t line_bytes, uint64_t cache_capacity, uint64_t cache_line,
+                                gnna_cost* cost) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        gnna::validate_params(p);
+        if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        cudaStream_t s = ctx->stream;
+        const uint64_t nnz = h_row_ptr[n];
+        const size_t elem = dtype == GNNA_F32 ? 4 : 8;
+        const size_t fbytes = (size_t)n * p->dim * elem;
+        gnna::DevBuf<uint64_t> rp((uint64_t)n + 1, s);
+        gnna::DevBuf<uint32_t> col(nnz ? nnz : 1, s);
+        gnna::DevBuf<uint8_t> x(fbytes ? fbytes : 1, s), y(fbytes ? fbytes : 1, s);
+        GNNA_CUDA(cudaMemcpyAsync(rp.get(), h_row_ptr, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (nnz) GNNA_CUDA(cudaMemcpyAsync(col.get(), h_col, nnz * 4, cudaMemcpyHostToDevice, s));
+        if (fbytes) GNNA_CUDA(cudaMemcpyAsync(x.get(), h_x, fbytes, cudaMemcpyHostToDevice, s));
+        gnna_plan* plan = nullptr;
+        gnna_status st = gnna_plan_create(ctx, rp.get(), col.get(), n, 0, n, p, strategy, &plan);
+        if (st != GNNA_OK) gnna::raise(st, ctx->err);
+        try {
+            gnna::aggregate_plan(ctx, plan, dtype, dim_mode, x.get(), y.get(), 0, nullptr, 0.0);
+            if (cost) gnna::cost_report(ctx, plan, dim_mode, line_bytes, cache_capacity, cache_line, cost);
+            if (fbytes) GNNA_CUDA(cudaMemcpyAsync(h_y, y.get(), fbytes, cudaMemcpyDeviceToHost, s));
+            GNNA_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            gnna_plan_destroy(plan);
+            throw;
+        }
+        gnna_plan_destroy(plan);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,149 @@
+// Shared internals of libgnna (the CUDA side of include/gnna.h).  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "gnna.h"
+
+struct gnna_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    int num_sms = 148;
+    int l2_bytes = 0;
+    int smem_optin = 0;
+};
+
+namespace gnna {
+
+// Thrown inside entry points; converted to a status by `guard`.
+struct Error {
+    gnna_status code;
+    std::string msg;
+};
+
+[[noreturn]] inline void raise(gnna_status code, std::string msg) { throw Error{code, std::move(msg)}; }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) raise(GNNA_ERR_OOM, std::string(what) + ": out of device memory");
+    raise(GNNA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define GNNA_CUDA(call) ::gnna::cuda_check((call), #call)
+
+// Record + check a kernel launch on ctx.
+inline void launched(gnna_ctx* ctx, const char* name) {
+    ctx->launches++;
+    cuda_check(cudaGetLastError(), name);
+}
+
+template <class F>
+gnna_status guard(gnna_ctx* ctx, F&& f) {
+    try {
+        f();
+        return GNNA_OK;
+    } catch (const Error& e) {
+        if (ctx) ctx->err = e.msg;
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return GNNA_ERR_INTERNAL;
+    }
+}
+
+inline void require_ctx(gnna_ctx* ctx) {
+    if (!ctx) raise(GNNA_ERR_DOMAIN, "null gnna_ctx");
+}
+
+// Stream-ordered scratch buffer (cudaMallocAsync pool).
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t count, cudaStream_t stream) : n(count), s(stream) {
+        if (count) GNNA_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p; n = o.n; s = o.s;
+            o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+};
+
+inline unsigned grid_for(uint64_t work, unsigned block, uint64_t cap = 1u << 20) {
+    uint64_t g = (work + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g);
+}
+
+template <class T>
+inline void to_host(gnna_ctx* ctx, T* host, const T* dev, size_t count) {
+    if (!count) return;
+    GNNA_CUDA(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    GNNA_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// Exclusive scan (u64) over `count` values in place-compatible buffers; returns total.
+uint64_t exclusive_scan_u64(gnna_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, uint64_t count);
+uint64_t exclusive_scan_u32_to_u64(gnna_ctx* ctx, const uint32_t* d_in, uint64_t* d_out, uint64_t count);
+uint64_t reduce_sum_u64(gnna_ctx* ctx, const uint64_t* d_in, uint64_t count);
+void sort_pairs_u64_u32(gnna_ctx* ctx, uint64_t* keys, uint32_t* vals, uint64_t count, int end_bit);
+void sort_keys_u64(gnna_ctx* ctx, uint64_t* keys, uint64_t count, int end_bit);
+
+}  // namespace gnna
+
+// Internal plan (gnna_plan is opaque at the ABI).
+struct gnna_plan {
+    gnna_ctx* ctx = nullptr;
+    gnna_params params{};
+    int strategy = GNNA_WARP_SHARED;
+    uint32_t n = 0, row_begin = 0, row_end = 0;
+    uint32_t wpb = 1;            // Algorithm-1 block width (tpb/32; 1 for Naive/UnitSync flush)
+    uint32_t wpb_params = 1;     // tpb/32 from params (counters use this)
+    const uint64_t* row_ptr = nullptr;
+    const uint32_t* col = nullptr;
+    uint64_t G = 0;              // workload units
+    uint64_t runs = 0;           // Algorithm-1 runs (= leaders)
+    uint64_t nsplit = 0;         // nodes whose units span > 1 schedule block
+    uint64_t ncarry = 0;         // carried run partials
+    uint64_t nempty = 0;         // zero-degree rows in range
+    gnna::DevBuf<uint64_t> part_ptr;   // G+1
+    gnna::DevBuf<uint32_t> part2node;  // G
+    gnna::DevBuf<uint8_t> slot;        // G, Algorithm-1 slot
+    gnna::DevBuf<uint8_t> leader;      // G, Algorithm-1 leader flag
+    gnna::DevBuf<uint8_t> uflags;      // G, kernel run flags (see plan.cu)
+    gnna::DevBuf<uint32_t> cidx;       // G, carry index of a split run's leader
+    gnna::DevBuf<uint32_t> fix_nodes;  // nsplit + nempty: split nodes then empty rows
+    gnna::DevBuf<uint32_t> fix_first;  // nsplit: first carry index
+    gnna::DevBuf<uint32_t> fix_count;  // nsplit: carries per split node
+    gnna::DevBuf<uint8_t> carry;       // ncarry * dim * 8 bytes
+};
+
+// Unit flag bits (plan.cu builds them, aggregate.cu consumes them).
+enum : uint8_t {
+    UF_LEADER = 1,     // first unit of an Algorithm-1 run
+    UF_RUN_END = 2,    // last unit of its run
+    UF_SPLIT = 4,      // the unit's node spans more than one schedule block
+};
