@@ -1,0 +1,421 @@
+"""Benchmark of the GNNAdvisor aggregation hot path on B200.
+
+Metric (BASELINE.json): aggregation edges x dim / s, with the HBM roofline
+fraction of the aggregation kernel.  A "step" is one scheduled aggregation
+(aggregate_scheduled, engine.cpp:200-311: K3 + the K3b carry combine) of a
+device-resident fp32 feature matrix over the workload graph; with N > 1 ranks
+each rank owns a contiguous nnz-balanced row range and the step
+ends with the all-gather of output rows (NCCL).  Default workload: C5 (10M
+nodes, ~200M nnz, dim 128), whose inputs (x = 5.1 GB) are far larger than L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c4|c3|c2|c1]
+  python bench.py --impl reference ...   # the reference's own CPU aggregate_scheduled
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "aggregation edges x dim / s"
+UNIT = "edge*dim/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--ngs", type=int, default=0)
+    ap.add_argument("--dw", type=int, default=0)
+    ap.add_argument("--tpb", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-nodes", type=int, default=0, help="CPU-baseline sample size (nodes)")
+    ap.add_argument("--flush-l2", action="store_true", help="force an L2 flush between steps")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- helpers
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) >= 8 and f[0].replace(".", "").isdigit():
+                    rows.append(f)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def cpu_sample(cfg, n_nodes, seed_offset=0):
+    """A bounded sample of the same workload for the CPU reference: the same
+    generator and mean degree at n_nodes, canonicalised by the reference's
+    own to_csr; fp64 U[0,1) features."""
+    import torch
+    from oracle.cpu import Oracle
+    from paper_2006_06608_b200 import synth
+    ref = Oracle("ref")
+    n, nnz = synth.scaled_config(cfg, n_nodes)
+
+    def to_csr(nn, e):
+        rp, col = ref.to_csr(nn, e.numpy().astype(np.uint32), True)
+        return rp, torch.from_numpy(col.view(np.int32))
+
+    edges, rp, col = synth.build_graph(cfg, to_csr, "cpu", n=n, nnz=nnz)
+    col = col.numpy().view(np.uint32)
+    x = np.random.default_rng(cfg.seed + seed_offset).random((n, cfg.dim))
+    return ref, rp, col, x
+
+
+def time_reference(ref, rp, col, x, params, workers, reps):
+    import ctypes as C
+    f = ref.lib.ref_time_aggregate_scheduled
+    f.restype = C.c_int
+    p = np.asarray(params, dtype=np.uint32)
+    secs = C.c_double()
+    n = len(rp) - 1
+    rc = f(C.c_uint32(n), C.c_void_p(rp.ctypes.data), C.c_void_p(col.ctypes.data), C.c_void_p(x.ctypes.data),
+           C.c_void_p(p.ctypes.data), C.c_int(2), C.c_int(1), C.c_uint32(workers), C.c_uint32(reps),
+           C.c_void_p(0), C.byref(secs))
+    if rc != 0:
+        raise RuntimeError("reference aggregate_scheduled failed: " + ref._err().decode())
+    return secs.value / reps
+
+
+def default_cpu_nodes(cfg):
+    # ~1-3 s per reference call on an 8+ core host
+    return min(cfg.n, {16: 400_000, 64: 150_000, 128: 200_000}.get(cfg.dim, 150_000))
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    from paper_2006_06608_b200 import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.workload]
+    nodes = args.cpu_nodes or default_cpu_nodes(cfg)
+    ref, rp, col, x = cpu_sample(cfg, nodes)
+    workers = os.cpu_count() or 1
+    params = [args.ngs or 256, args.dw or 32, args.tpb or 128, 32, cfg.dim]
+    nnz = int(rp[-1])
+    for _ in range(args.warmup):
+        time_reference(ref, rp, col, x, params, workers, 1)
+    times = [time_reference(ref, rp, col, x, params, workers, 1) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = nnz * cfg.dim / t
+    sample = f"{cfg.name} generator at n={len(rp) - 1}, nnz={nnz}, d={cfg.dim}, fp64 (reference FeatureMatrix)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "sample_nodes": len(rp) - 1, "sample_nnz": nnz, "dim": cfg.dim,
+                   "params": {"ngs": params[0], "dw": params[1], "tpb": params[2]},
+                   "strategy": "WarpShared", "dim_mode": "Cyclic"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2006_06608_b200 import synth
+    from paper_2006_06608_b200.capi import WARP_SHARED, Context, Params
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(local, stream)
+    cfg = synth.CONFIGS[args.workload]
+
+    t0 = time.time()
+    edges, rp, col = synth.build_graph(cfg, lambda n, e: ctx.to_csr(n, e, True), dev)
+    del edges
+    n = cfg.n
+    nnz = int(col.numel())
+    x = synth.features(n, cfg.dim, cfg.seed, dev)
+    y = torch.zeros_like(x)
+    rp_host = rp.cpu().numpy().view(np.uint64)
+    ranges = synth.balanced_rows(rp_host, world)
+    r0, r1 = ranges[rank]
+    my_nnz = int(rp_host[r1] - rp_host[r0])
+    gen_s = time.time() - t0
+
+    # Parameters: the performance evaluator with the B200 profile, unless overridden.
+    mi = ctx.model_inputs(rp, cfg.dim, b200=True)
+    p = ctx.auto_params(mi)
+    if args.ngs:
+        p.ngs = args.ngs
+    if args.dw:
+        p.dw = args.dw
+    if args.tpb:
+        p.tpb = args.tpb
+    t1 = time.time()
+    plan = ctx.plan(rp, col, p, WARP_SHARED, rows=(r0, r1))
+    torch.cuda.synchronize()
+    plan_s = time.time() - t1
+
+    x_bytes = x.numel() * 4
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = args.flush_l2 or x_bytes < 4 * l2
+    scratch = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev) if flush else None
+    views = [y[a:b] for a, b in ranges]
+
+    def step():
+        plan.aggregate(x, out=y)
+        if world > 1:
+            dist.all_gather(views, views[rank].contiguous())
+
+    for _ in range(args.warmup):
+        step()
+        if flush:
+            scratch.fill_(1.0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launches
+    with Clocks(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            a, b, c = ev[i]
+            a.record(stream)
+            plan.aggregate(x, out=y)
+            b.record(stream)
+            if world > 1:
+                dist.all_gather(views, views[rank].contiguous())
+            c.record(stream)
+            if flush:
+                scratch.fill_(1.0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = ctx.launches - launches0
+    step_ms = [a.elapsed_time(c) for a, _, c in ev]
+    agg_ms = [a.elapsed_time(b) for a, b, _ in ev]
+    t_step = sum(step_ms) / len(step_ms)
+    t_agg = sum(agg_ms) / len(agg_ms)
+    if world > 1:
+        tt = torch.tensor([t_step, t_agg], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_agg = float(tt[0]), float(tt[1])
+    clocks = clk.summary()
+
+    value = nnz * cfg.dim / (t_step * 1e-3)
+    balg_rank = synth.b_alg(r1 - r0, my_nnz, cfg.dim)
+    peak, peak_src = peaks()
+    achieved = balg_rank / (t_agg * 1e-3) / 1e9
+
+    # correctness spot check of this run against the CPU oracle on sampled rows
+    check = spot_check(rp_host, col, x, y, ranges if world > 1 else [(r0, r1)], cfg.dim)
+
+    # ---------------- e2e through the host-buffer C-ABI entry (pinned buffers)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(ctx, rp, col, x, p, r0, r1, cfg, args, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            nodes = args.cpu_nodes or default_cpu_nodes(cfg)
+            ref, srp, scol, sx = cpu_sample(cfg, nodes)
+            workers = os.cpu_count() or 1
+            reps = 2
+            ts = time_reference(ref, srp, scol, sx, [p.ngs, p.dw, p.tpb, 32, cfg.dim], workers, reps)
+            snnz = int(srp[-1])
+            cpu = {"value": snnz * cfg.dim / ts, "unit": UNIT, "cores": workers, "kind": "reference",
+                   "sample": f"reference aggregate_scheduled (WarpShared, Cyclic, fp64, workers={workers}) on "
+                             f"{cfg.name} generator at n={len(srp) - 1}, nnz={snnz}, d={cfg.dim}; "
+                             f"mean of {reps} calls ({ts:.2f} s each)"}
+        except Exception as exc:  # the baseline is reported, not required
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": n, "nnz": nnz, "dim": cfg.dim,
+                       "params": {"ngs": p.ngs, "dw": p.dw, "tpb": p.tpb, "tpw": p.tpw},
+                       "strategy": "WarpShared", "dim_mode": "Cyclic", "parallelism": f"rows{world}",
+                       "l2": "flushed between steps" if flush else f"inputs ({x_bytes / 1e9:.2f} GB x) > L2 ({l2 / 1e6:.0f} MB)",
+                       "plan": plan.info(), "graph_build_s": round(gen_s, 3), "plan_build_s": round(plan_s, 3),
+                       "max_degree": int(np.diff(rp_host).max())},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "kernel": "k3_aggregate (+k3b_fixup)", "kernel_ms": t_agg,
+                         "algorithmic_bytes_per_launch": balg_rank},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "parity": check,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def spot_check(rp_host, col, x, y, ranges, dim, rows=2000):
+    """fp32 result vs an fp64 CSR-order sum on sampled rows (rel. 1e-5)."""
+    rng = np.random.default_rng(0)
+    col_h = None
+    worst = 0.0
+    for a, b in ranges:
+        if b <= a:
+            continue
+        pick = np.unique(np.concatenate([rng.integers(a, b, size=rows), [a, b - 1]]))
+        if col_h is None:
+            col_h = col.cpu().numpy().view(np.uint32)
+        x_rows = {}
+        ys = y[torch_index(pick, y.device)].cpu().numpy().astype(np.float64)
+        for k, v in enumerate(pick):
+            nb = col_h[rp_host[v]:rp_host[v + 1]]
+            if len(nb) == 0:
+                want = np.zeros(dim)
+            else:
+                xs = x[torch_index(nb, x.device)].cpu().numpy().astype(np.float64)
+                want = xs.sum(0)
+            err = np.abs(ys[k] - want) / np.maximum(np.abs(want), 1e-30)
+            err[np.abs(ys[k] - want) == 0] = 0
+            worst = max(worst, float(err.max()) if err.size else 0.0)
+        del x_rows
+    return {"rows_checked": rows * len(ranges), "max_rel_err": worst, "tol": 1e-5, "ok": worst <= 1e-5}
+
+
+def torch_index(idx, device):
+    import torch
+    return torch.from_numpy(np.asarray(idx, dtype=np.int64)).to(device)
+
+
+def run_e2e(ctx, rp, col, x, p, r0, r1, cfg, args, world, dev):
+    """Same metric through gnna_aggregate_host: pinned HOST CSR + features in,
+    host output rows back; H2D/D2H copies, planning and the kernels inside the
+    timed region (what a drop-in aggregate_scheduled call does)."""
+    import torch
+    import torch.distributed as dist
+    h_rp = rp.cpu().pin_memory()
+    h_col = col.cpu().pin_memory()
+    h_x = x.cpu().pin_memory()
+    rows = r1 - r0
+    h_y = torch.empty((rows, cfg.dim), dtype=torch.float32).pin_memory()
+    steps = max(1, min(args.steps, 5))
+
+    def call():
+        ctx.aggregate_host_rows(h_rp, h_col, h_x, p, r0, r1, h_y)
+
+    call()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    t = (time.perf_counter() - t0) / steps
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt[0])
+    nnz = int(col.numel())
+    h2d = h_rp.numel() * 8 + h_col.numel() * 4 + h_x.numel() * 4
+    d2h = h_y.numel() * 4
+    return {"value": nnz * cfg.dim / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": t * 1e3, "steps": steps,
+            "path": "gnna_aggregate_host (C-ABI, host buffers; upload + plan + K3 + download)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -157,6 +157,18 @@ GNNA_API gnna_status gnna_aggregate_host(gnna_ctx* ctx, int dtype, const uint64_
                                 uint64_t line_bytes, uint64_t cache_capacity,
                                 uint64_t cache_line, gnna_cost* cost);
 
+/* Row-shard variant (multi-GPU row sharding): rows
+ * [row_begin, row_end) of the host CSR are aggregated over the full host
+ * feature matrix; only the shard's CSR slice is uploaded and h_y receives
+ * (row_end - row_begin) x dim values.  The cost report (when requested)
+ * describes the shard's own schedule. */
+GNNA_API gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr,
+                                     const uint32_t* h_col, uint32_t n, uint32_t row_begin,
+                                     uint32_t row_end, const gnna_params* p, int strategy,
+                                     int dim_mode, const void* h_x, void* h_y,
+                                     uint64_t line_bytes, uint64_t cache_capacity,
+                                     uint64_t cache_line, gnna_cost* cost);
+
 /* -------------------------------------------------------- GCN / GIN --- */
 /* engine.cpp:340-353: norm[v] = 1/sqrt(max(deg'(v),1)) (f64), deg' counts an
  * implicit self loop when add_self_loops and v has none; d_self (u8, may be

@@ -9,6 +9,7 @@
 //
 // Status codes: 0 ok, 1 DomainError, 2 InternalError, 3 ParseError,
 // 4 IoError, 5 other std::exception, 6 caller buffer too small.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -495,6 +496,57 @@ int ref_search_params(const PodInputs* in, uint32_t iterations, uint32_t populat
         *trace_len = static_cast<uint32_t>(tr.best_per_iteration.size());
         for (size_t i = 0; i < tr.best_per_iteration.size(); ++i)
             trace[i] = tr.best_per_iteration[i];
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+// CPU baseline for bench.py: builds the reference value types once, then times
+// `reps` calls of the reference's own aggregate_scheduled (engine.cpp:200)
+// with std::chrono::steady_clock; only the reference call is inside the clock.
+int ref_time_aggregate_scheduled(uint32_t n, const uint64_t* row_ptr, const uint32_t* col,
+                                 const double* x, const uint32_t p[5], int strategy,
+                                 int dim_mode, uint32_t workers, uint32_t reps,
+                                 double* y, double* seconds) {
+    return guard([&] {
+        const KernelParams k = view_params(p);
+        EngineOptions opts;
+        opts.workers = workers;
+        opts.cache.reset();
+        const Strategy s = strategy == 0   ? Strategy::NaiveAtomic
+                           : strategy == 1 ? Strategy::UnitSync
+                                           : Strategy::WarpShared;
+        const CsrGraph g = view_csr(n, row_ptr, col);
+        const FeatureMatrix fx = view_fm(n, k.dim, x);
+        const auto mode = dim_mode == 0 ? DimMode::Sequential : DimMode::Cyclic;
+        double total = 0.0;
+        for (uint32_t r = 0; r < reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const auto [out, rep] = aggregate_scheduled(g, fx, k, s, mode, opts);
+            const auto t1 = std::chrono::steady_clock::now();
+            total += std::chrono::duration<double>(t1 - t0).count();
+            if (r + 1 == reps && y)
+                std::memcpy(y, out.values.data(), sizeof(double) * out.values.size());
+        }
+        *seconds = total;
+    });
+}
+
+// Same for aggregate_oracle (engine.cpp:149), single-threaded by design.
+int ref_time_aggregate_oracle(uint32_t n, const uint64_t* row_ptr, const uint32_t* col,
+                              const double* x, uint32_t dim, uint32_t reps, double* seconds) {
+    return guard([&] {
+        const CsrGraph g = view_csr(n, row_ptr, col);
+        const FeatureMatrix fx = view_fm(n, dim, x);
+        double total = 0.0;
+        for (uint32_t r = 0; r < reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const FeatureMatrix out = aggregate_oracle(g, fx);
+            const auto t1 = std::chrono::steady_clock::now();
+            total += std::chrono::duration<double>(t1 - t0).count();
+        }
+        *seconds = total;
     });
 }
 

@@ -214,6 +214,57 @@ class Context:
                                                C.byref(cost) if want_cost else None))
         return out, cost
 
+    # --------------------------------------------------------------- graph
+    def to_csr(self, n, edges, symmetrize=True):
+        """graph.cpp:76 to_csr on the GPU: edges (E,2) int32 device tensor ->
+        (row_ptr int64[n+1], col int32[nnz]) canonical CSR."""
+        torch = self.torch
+        e = edges.numel() // 2
+        nnz = C.c_uint64()
+        rp = self._empty(n + 1, torch.int64)
+        self._check(self.L.gnna_to_csr(self.h, C.c_uint32(n), _ptr(edges), C.c_uint64(e), C.c_int(int(symmetrize)),
+                                       _ptr(rp), C.c_void_p(0), C.byref(nnz)))
+        col = self._empty(max(nnz.value, 1), torch.int32)
+        self._check(self.L.gnna_to_csr(self.h, C.c_uint32(n), _ptr(edges), C.c_uint64(e), C.c_int(int(symmetrize)),
+                                       _ptr(rp), _ptr(col), C.byref(nnz)))
+        return rp, col[: nnz.value]
+
+    def csr_transpose(self, row_ptr, col):
+        n = row_ptr.numel() - 1
+        tp = self._empty(n + 1, self.torch.int64)
+        tc = self._empty(max(col.numel(), 1), self.torch.int32)
+        self._check(self.L.gnna_csr_transpose(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), _ptr(tp), _ptr(tc)))
+        return tp, tc[: col.numel()]
+
+    def aes(self, edges):
+        out = C.c_double()
+        self._check(self.L.gnna_aes(self.h, _ptr(edges), C.c_uint64(edges.numel() // 2), C.byref(out)))
+        return out.value
+
+    def degree_stats(self, row_ptr):
+        a, m, s = C.c_double(), C.c_uint64(), C.c_double()
+        self._check(self.L.gnna_degree_stats(self.h, _ptr(row_ptr), C.c_uint32(row_ptr.numel() - 1), C.byref(a),
+                                             C.byref(m), C.byref(s)))
+        return a.value, m.value, s.value
+
+    def model_inputs(self, row_ptr, dim, b200=False):
+        mi = ModelInputs()
+        self._check(self.L.gnna_model_inputs_from_graph(self.h, _ptr(row_ptr), C.c_uint32(row_ptr.numel() - 1),
+                                                        C.c_uint32(dim), C.byref(mi)))
+        if b200:
+            self._check(self.L.gnna_b200_profile(self.h, C.byref(mi)))
+        return mi
+
+    def aggregate_host_rows(self, row_ptr, col, x, p: Params, r0, r1, out, strategy=WARP_SHARED,
+                            dim_mode=DIM_CYCLIC):
+        """gnna_aggregate_host_rows over host (pinned) torch tensors; out: (r1-r0) x dim."""
+        n = row_ptr.numel() - 1
+        self._check(self.L.gnna_aggregate_host_rows(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col),
+                                                    C.c_uint32(n), C.c_uint32(r0), C.c_uint32(r1), C.byref(p),
+                                                    C.c_int(strategy), C.c_int(dim_mode), _ptr(x), _ptr(out),
+                                                    C.c_uint64(128), C.c_uint64(0), C.c_uint64(0), None))
+        return out
+
     # ------------------------------------------------------------- decider
     def auto_params(self, inputs: ModelInputs) -> Params:
         p = Params()

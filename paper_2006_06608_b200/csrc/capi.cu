@@ -9,6 +9,7 @@ void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mod
                     uint32_t epi, const float* scale, double alpha);
 void cost_report(gnna_ctx* ctx, const gnna_plan* plan, int dim_mode, uint64_t line, uint64_t cache_cap,
                  uint64_t cache_line, gnna_cost* out);
+void rebase_u64(gnna_ctx* ctx, uint64_t* v, uint64_t count, uint64_t base);
 }  // namespace gnna
 
 extern "C" {
@@ -59,31 +60,38 @@ const char* gnna_last_error(const gnna_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 uint64_t gnna_launch_count(const gnna_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-gnna_status gnna_aggregate_host(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr, const uint32_t* h_col,
-                                uint32_t n, const gnna_params* p, int strategy, int dim_mode, const void* h_x,
-                                void* h_y, uint64_t line_bytes, uint64_t cache_capacity, uint64_t cache_line,
-                                gnna_cost* cost) {
+gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr, const uint32_t* h_col,
+                                     uint32_t n, uint32_t row_begin, uint32_t row_end, const gnna_params* p,
+                                     int strategy, int dim_mode, const void* h_x, void* h_y, uint64_t line_bytes,
+                                     uint64_t cache_capacity, uint64_t cache_line, gnna_cost* cost) {
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
         gnna::validate_params(p);
         if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        if (row_begin > row_end || row_end > n) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_host: bad row range");
         cudaStream_t s = ctx->stream;
-        const uint64_t nnz = h_row_ptr[n];
+        const uint32_t rows = row_end - row_begin;
+        const uint64_t e0 = h_row_ptr[row_begin], e1 = h_row_ptr[row_end];
+        const uint64_t nnz = e1 - e0;
         const size_t elem = dtype == GNNA_F32 ? 4 : 8;
-        const size_t fbytes = (size_t)n * p->dim * elem;
-        gnna::DevBuf<uint64_t> rp((uint64_t)n + 1, s);
+        const size_t xbytes = (size_t)n * p->dim * elem;
+        const size_t ybytes = (size_t)rows * p->dim * elem;
+        // The shard is a rows x n CSR: its own rebased row_ptr and column
+        // slice, gathering from the full (replicated) feature matrix.
+        gnna::DevBuf<uint64_t> rp((uint64_t)rows + 1, s);
         gnna::DevBuf<uint32_t> col(nnz ? nnz : 1, s);
-        gnna::DevBuf<uint8_t> x(fbytes ? fbytes : 1, s), y(fbytes ? fbytes : 1, s);
-        GNNA_CUDA(cudaMemcpyAsync(rp.get(), h_row_ptr, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, s));
-        if (nnz) GNNA_CUDA(cudaMemcpyAsync(col.get(), h_col, nnz * 4, cudaMemcpyHostToDevice, s));
-        if (fbytes) GNNA_CUDA(cudaMemcpyAsync(x.get(), h_x, fbytes, cudaMemcpyHostToDevice, s));
+        gnna::DevBuf<uint8_t> x(xbytes ? xbytes : 1, s), y(ybytes ? ybytes : 1, s);
+        GNNA_CUDA(cudaMemcpyAsync(rp.get(), h_row_ptr + row_begin, ((size_t)rows + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (e0) gnna::rebase_u64(ctx, rp.get(), (uint64_t)rows + 1, e0);
+        if (nnz) GNNA_CUDA(cudaMemcpyAsync(col.get(), h_col + e0, nnz * 4, cudaMemcpyHostToDevice, s));
+        if (xbytes) GNNA_CUDA(cudaMemcpyAsync(x.get(), h_x, xbytes, cudaMemcpyHostToDevice, s));
         gnna_plan* plan = nullptr;
-        gnna_status st = gnna_plan_create(ctx, rp.get(), col.get(), n, 0, n, p, strategy, &plan);
+        gnna_status st = gnna_plan_create(ctx, rp.get(), col.get(), rows, 0, rows, p, strategy, &plan);
         if (st != GNNA_OK) gnna::raise(st, ctx->err);
         try {
             gnna::aggregate_plan(ctx, plan, dtype, dim_mode, x.get(), y.get(), 0, nullptr, 0.0);
             if (cost) gnna::cost_report(ctx, plan, dim_mode, line_bytes, cache_capacity, cache_line, cost);
-            if (fbytes) GNNA_CUDA(cudaMemcpyAsync(h_y, y.get(), fbytes, cudaMemcpyDeviceToHost, s));
+            if (ybytes) GNNA_CUDA(cudaMemcpyAsync(h_y, y.get(), ybytes, cudaMemcpyDeviceToHost, s));
             GNNA_CUDA(cudaStreamSynchronize(s));
         } catch (...) {
             gnna_plan_destroy(plan);
@@ -91,6 +99,14 @@ gnna_status gnna_aggregate_host(gnna_ctx* ctx, int dtype, const uint64_t* h_row_
         }
         gnna_plan_destroy(plan);
     });
+}
+
+gnna_status gnna_aggregate_host(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr, const uint32_t* h_col,
+                                uint32_t n, const gnna_params* p, int strategy, int dim_mode, const void* h_x,
+                                void* h_y, uint64_t line_bytes, uint64_t cache_capacity, uint64_t cache_line,
+                                gnna_cost* cost) {
+    return gnna_aggregate_host_rows(ctx, dtype, h_row_ptr, h_col, n, 0, n, p, strategy, dim_mode, h_x, h_y,
+                                    line_bytes, cache_capacity, cache_line, cost);
 }
 
 }  // extern "C"

@@ -7,7 +7,20 @@
 
 #include "gnna_common.cuh"
 
+namespace {
+__global__ void k_rebase_u64(uint64_t* v, uint64_t count, uint64_t base) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+        v[i] -= base;
+}
+}  // namespace
+
 namespace gnna {
+
+void rebase_u64(gnna_ctx* ctx, uint64_t* v, uint64_t count, uint64_t base) {
+    if (!count) return;
+    k_rebase_u64<<<grid_for(count, 256), 256, 0, ctx->stream>>>(v, count, base);
+    launched(ctx, "k_rebase_u64");
+}
 
 uint64_t exclusive_scan_u64(gnna_ctx* ctx, const uint64_t* d_in, uint64_t* d_out, uint64_t count) {
     // d_out has count+1 entries; d_out[count] = total.
