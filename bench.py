@@ -196,7 +196,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2006_06608_b200 import synth
-    from paper_2006_06608_b200.capi import WARP_SHARED, Context, Params
+    from paper_2006_06608_b200.capi import WARP_SHARED, Context
+    from paper_2006_06608_b200.shard import allgather_rows, row_ranges
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -217,7 +218,7 @@ def run_ours(args):
     x = synth.features(n, cfg.dim, cfg.seed, dev)
     y = torch.zeros_like(x)
     rp_host = rp.cpu().numpy().view(np.uint64)
-    ranges = synth.balanced_rows(rp_host, world)
+    ranges = row_ranges(rp_host, world)
     r0, r1 = ranges[rank]
     my_nnz = int(rp_host[r1] - rp_host[r0])
     gen_s = time.time() - t0
@@ -240,12 +241,11 @@ def run_ours(args):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = args.flush_l2 or x_bytes < 4 * l2
     scratch = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev) if flush else None
-    views = [y[a:b] for a, b in ranges]
 
     def step():
         plan.aggregate(x, out=y)
         if world > 1:
-            dist.all_gather(views, views[rank].contiguous())
+            allgather_rows(y, ranges, rank)
 
     for _ in range(args.warmup):
         step()
@@ -268,7 +268,7 @@ def run_ours(args):
             plan.aggregate(x, out=y)
             b.record(stream)
             if world > 1:
-                dist.all_gather(views, views[rank].contiguous())
+                allgather_rows(y, ranges, rank)
             c.record(stream)
             if flush:
                 scratch.fill_(1.0)

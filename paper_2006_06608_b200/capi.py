@@ -265,6 +265,123 @@ class Context:
                                                     C.c_uint64(128), C.c_uint64(0), C.c_uint64(0), None))
         return out
 
+    # ------------------------------------------------------- layers (K5/K6)
+    def gemm(self, a, w, bias=None, epilogue=0, row_scale=None, out=None):
+        m, k = a.shape
+        n_out = w.shape[1]
+        if out is None:
+            out = self.torch.empty((m, n_out), dtype=a.dtype, device=a.device)
+        self._check(self.L.gnna_gemm(self.h, C.c_int(_dtype_code(a)), _ptr(a), C.c_uint32(m), C.c_uint32(k), _ptr(w),
+                                     C.c_uint32(n_out), _ptr(bias), C.c_int(epilogue), _ptr(row_scale), _ptr(out)))
+        return out
+
+    def gcn_norm(self, row_ptr, col, self_loops=False):
+        n = row_ptr.numel() - 1
+        norm = self._empty(max(n, 1), self.torch.float64)
+        sl = self._empty(max(n, 1), self.torch.uint8)
+        self._check(self.L.gnna_gcn_norm(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), C.c_int(int(self_loops)),
+                                         _ptr(norm), _ptr(sl)))
+        return norm[:n], sl[:n]
+
+    def normalized_aggregate(self, row_ptr, col, x, norm, selfl, out=None):
+        n = row_ptr.numel() - 1
+        if out is None:
+            out = self.torch.empty_like(x)
+        self._check(self.L.gnna_normalized_aggregate(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col),
+                                                     C.c_uint32(n), C.c_uint32(x.shape[1]), _ptr(norm), _ptr(selfl),
+                                                     _ptr(x), _ptr(out)))
+        return out
+
+    def gcn_forward(self, row_ptr, col, x, w, self_loops=False):
+        n = row_ptr.numel() - 1
+        y = self.torch.empty((n, w.shape[1]), dtype=x.dtype, device=x.device)
+        self._check(self.L.gnna_gcn_forward(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col), C.c_uint32(n),
+                                            _ptr(x), C.c_uint32(x.shape[1]), _ptr(w), C.c_uint32(w.shape[1]),
+                                            C.c_int(int(self_loops)), _ptr(y)))
+        return y
+
+    def gin_forward(self, row_ptr, col, x, eps, w, b):
+        n = row_ptr.numel() - 1
+        y = self.torch.empty((n, w.shape[1]), dtype=x.dtype, device=x.device)
+        self._check(self.L.gnna_gin_forward(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col), C.c_uint32(n),
+                                            _ptr(x), C.c_uint32(x.shape[1]), C.c_double(eps), _ptr(w),
+                                            C.c_uint32(w.shape[1]), _ptr(b), _ptr(y)))
+        return y
+
+    def gcn_backward(self, row_ptr, col, x, w, dy, self_loops=False, rt=None):
+        n = row_ptr.numel() - 1
+        rtp, rtc = rt if rt is not None else (row_ptr, col)
+        dx = self.torch.empty_like(x)
+        dw = self.torch.empty_like(w)
+        self._check(self.L.gnna_gcn_backward(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col), _ptr(rtp),
+                                             _ptr(rtc), C.c_uint32(n), _ptr(x), C.c_uint32(x.shape[1]), _ptr(w),
+                                             C.c_uint32(w.shape[1]), C.c_int(int(self_loops)), _ptr(dy), _ptr(dx),
+                                             _ptr(dw)))
+        return dx, dw
+
+    def gin_backward(self, row_ptr, col, x, eps, w, b, dy, rt=None):
+        n = row_ptr.numel() - 1
+        rtp, rtc = rt if rt is not None else (row_ptr, col)
+        dx, dw, db = self.torch.empty_like(x), self.torch.empty_like(w), self.torch.empty_like(b)
+        de = C.c_double()
+        self._check(self.L.gnna_gin_backward(self.h, C.c_int(_dtype_code(x)), _ptr(row_ptr), _ptr(col), _ptr(rtp),
+                                             _ptr(rtc), C.c_uint32(n), _ptr(x), C.c_uint32(x.shape[1]),
+                                             C.c_double(eps), _ptr(w), C.c_uint32(w.shape[1]), _ptr(b), _ptr(dy),
+                                             _ptr(dx), _ptr(dw), _ptr(db), C.byref(de)))
+        return dx, dw, db, de.value
+
+    # ----------------------------------------------------------- renumber
+    def detect_communities(self, row_ptr, col):
+        n = row_ptr.numel() - 1
+        com = self._empty(max(n, 1), self.torch.int32)
+        k = C.c_uint32()
+        self._check(self.L.gnna_detect_communities(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), _ptr(com),
+                                                   C.byref(k)))
+        return com[:n], k.value
+
+    def modularity(self, row_ptr, col, com, ncom):
+        q = C.c_double()
+        self._check(self.L.gnna_modularity(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(row_ptr.numel() - 1),
+                                           _ptr(com), C.c_uint32(ncom), C.byref(q)))
+        return q.value
+
+    def build_mapping(self, com, ncom):
+        n = com.numel()
+        o2n, n2o = self._empty(max(n, 1), self.torch.int32), self._empty(max(n, 1), self.torch.int32)
+        self._check(self.L.gnna_build_mapping(self.h, _ptr(com), C.c_uint32(n), C.c_uint32(ncom), _ptr(o2n),
+                                              _ptr(n2o)))
+        return o2n[:n], n2o[:n]
+
+    def mapping_from_vector(self, vec):
+        n = vec.numel()
+        o2n, n2o = self._empty(max(n, 1), self.torch.int32), self._empty(max(n, 1), self.torch.int32)
+        self._check(self.L.gnna_mapping_from_vector(self.h, _ptr(vec), C.c_uint32(n), _ptr(o2n), _ptr(n2o)))
+        return o2n[:n], n2o[:n]
+
+    def apply_mapping_csr(self, row_ptr, col, o2n, n2o):
+        n = row_ptr.numel() - 1
+        orp = self._empty(n + 1, self.torch.int64)
+        oc = self._empty(max(col.numel(), 1), self.torch.int32)
+        self._check(self.L.gnna_apply_mapping_csr(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), _ptr(o2n),
+                                                  _ptr(n2o), _ptr(orp), _ptr(oc)))
+        return orp, oc[: col.numel()]
+
+    def apply_mapping_edges(self, edges, n, o2n):
+        out = self.torch.empty_like(edges)
+        self._check(self.L.gnna_apply_mapping_edges(self.h, _ptr(edges), C.c_uint64(edges.numel() // 2),
+                                                    C.c_uint32(n), _ptr(o2n), _ptr(out)))
+        return out
+
+    def tune_params(self, row_ptr, col, dim, gs=(1, 2, 4, 8, 16, 32, 64, 128, 256), dw=(4, 8, 16, 32),
+                    tpb=(32, 64, 128, 256)):
+        g, d, t = (np.asarray(v, np.uint32) for v in (gs, dw, tpb))
+        best = Params()
+        ms = C.c_float()
+        self._check(self.L.gnna_tune_params(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(row_ptr.numel() - 1),
+                                            C.c_uint32(dim), _ptr(g), C.c_uint32(len(g)), _ptr(d), C.c_uint32(len(d)),
+                                            _ptr(t), C.c_uint32(len(t)), C.byref(best), C.byref(ms)))
+        return best, ms.value
+
     # ------------------------------------------------------------- decider
     def auto_params(self, inputs: ModelInputs) -> Params:
         p = Params()
@@ -322,3 +439,61 @@ class Plan:
                                                        C.c_uint64(cache[1]), C.c_uint32(dim), C.byref(h),
                                                        C.byref(a)))
         return h.value, a.value
+
+
+# ------------------------------------------------- evaluator (host, no GPU)
+# decider.hpp:46-94: these run on the host inside libgnna.so and need no
+# device, so the CPU test suite checks them against the reference.
+class Decider:
+    def __init__(self):
+        self.L = lib()
+        self.L.gnna_alpha_from_degrees.restype = C.c_double
+
+    def _chk(self, rc, what):
+        if rc:
+            raise DomainError(rc, what)
+
+    def alpha_from_degrees(self, avg, sd):
+        return self.L.gnna_alpha_from_degrees(C.c_double(avg), C.c_double(sd))
+
+    def select_dw(self, dim, tpw=32):
+        out = C.c_uint32()
+        self._chk(self.L.gnna_select_dw(C.c_uint32(dim), C.c_uint32(tpw), C.byref(out)), "select_dw")
+        return out.value
+
+    def select_ngs(self, dw, tpb, inputs):
+        out = C.c_uint32()
+        self._chk(self.L.gnna_select_ngs(C.c_uint32(dw), C.c_uint32(tpb), C.byref(inputs), C.byref(out)), "select_ngs")
+        return out.value
+
+    def dp_size(self, smem, avg):
+        out = C.c_double()
+        self._chk(self.L.gnna_dp_size(C.c_uint64(smem), C.c_double(avg), C.byref(out)), "dp_size")
+        return out.value
+
+    def estimate_latency(self, p: Params, inputs):
+        out = C.c_double()
+        self._chk(self.L.gnna_estimate_latency(C.byref(p), C.byref(inputs), C.byref(out)), "estimate_latency")
+        return out.value
+
+    def feasible(self, p: Params, inputs):
+        return (bool(self.L.gnna_candidate_feasible(C.byref(p), C.byref(inputs))),
+                bool(self.L.gnna_feasibility(C.byref(p), C.byref(inputs))))
+
+    def auto_params(self, inputs) -> Params:
+        p = Params()
+        self._chk(self.L.gnna_auto_params(C.byref(inputs), C.byref(p)), "auto_params")
+        return p
+
+    def search_params(self, inputs, iterations=15, population=32, seed=1, gs=(1, 2, 4, 8, 16, 32, 64),
+                      dw=(8, 16, 32), tpb=(32, 64, 128, 256)):
+        g, d, t = (np.asarray(v, np.uint32) for v in (gs, dw, tpb))
+        best = Params()
+        lat, feas = C.c_double(), C.c_int()
+        trace = np.zeros(iterations + 1, np.float64)
+        tl = C.c_uint32()
+        self._chk(self.L.gnna_search_params(C.byref(inputs), C.c_uint32(iterations), C.c_uint32(population),
+                                            C.c_uint64(seed), _ptr(g), C.c_uint32(len(g)), _ptr(d), C.c_uint32(len(d)),
+                                            _ptr(t), C.c_uint32(len(t)), C.byref(best), C.byref(lat), C.byref(feas),
+                                            _ptr(trace), C.byref(tl)), "search_params")
+        return best, lat.value, bool(feas.value), trace[: tl.value].copy()

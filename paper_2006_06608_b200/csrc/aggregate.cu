@@ -520,3 +520,53 @@ gnna_status gnna_aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* d_row_
 }
 
 }  // extern "C"
+
+extern "C" gnna_status gnna_tune_params(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                                        uint32_t dim, const uint32_t* gs_values, uint32_t n_gs,
+                                        const uint32_t* dw_values, uint32_t n_dw, const uint32_t* tpb_values,
+                                        uint32_t n_tpb, gnna_params* best, float* best_ms) {
+    // Measured-latency evaluator: the analytic model of
+    // decider.cpp:70-81 replaced by CUDA-event timings of K3 on the live graph.
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (!best || !n_gs || !n_dw || !n_tpb) gnna::raise(GNNA_ERR_DOMAIN, "tune_params: empty grid");
+        cudaStream_t s = ctx->stream;
+        gnna::DevBuf<float> x((size_t)n * dim + 4, s), y((size_t)n * dim + 4, s);
+        GNNA_CUDA(cudaMemsetAsync(x.get(), 0, ((size_t)n * dim + 4) * 4, s));
+        cudaEvent_t e0, e1;
+        GNNA_CUDA(cudaEventCreate(&e0));
+        GNNA_CUDA(cudaEventCreate(&e1));
+        float best_t = 3.4e38f;
+        gnna_params bp{};
+        bool found = false;
+        for (uint32_t i = 0; i < n_gs; ++i)
+            for (uint32_t j = 0; j < n_dw; ++j)
+                for (uint32_t k = 0; k < n_tpb; ++k) {
+                    gnna_params p{gs_values[i], dw_values[j], tpb_values[k], 32, dim};
+                    gnna_plan* plan = nullptr;
+                    if (gnna_plan_create(ctx, d_row_ptr, d_col, n, 0, n, &p, GNNA_WARP_SHARED, &plan) != GNNA_OK)
+                        continue;  // infeasible combination (validate() domain)
+                    gnna::aggregate_plan(ctx, plan, GNNA_F32, GNNA_DIM_CYCLIC, x.get(), y.get(), 0, nullptr, 0.0);
+                    GNNA_CUDA(cudaEventRecord(e0, s));
+                    const int reps = 3;
+                    for (int r = 0; r < reps; ++r)
+                        gnna::aggregate_plan(ctx, plan, GNNA_F32, GNNA_DIM_CYCLIC, x.get(), y.get(), 0, nullptr, 0.0);
+                    GNNA_CUDA(cudaEventRecord(e1, s));
+                    GNNA_CUDA(cudaEventSynchronize(e1));
+                    float ms = 0;
+                    GNNA_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+                    ms /= reps;
+                    gnna_plan_destroy(plan);
+                    if (ms < best_t) {
+                        best_t = ms;
+                        bp = p;
+                        found = true;
+                    }
+                }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (!found) gnna::raise(GNNA_ERR_DOMAIN, "tune_params: no feasible combination");
+        *best = bp;
+        if (best_ms) *best_ms = best_t;
+    });
+}

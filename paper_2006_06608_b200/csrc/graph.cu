@@ -136,12 +136,21 @@ namespace gnna {
 
 // Sorted, de-duplicated CSR from u64 (row<<32|col) keys; keys is clobbered.
 // Returns nnz; col must hold `m` entries.
-uint64_t csr_from_keys(gnna_ctx* ctx, uint64_t* keys, uint64_t m, uint32_t n, uint64_t* row_ptr, uint32_t* col) {
+uint64_t csr_from_keys(gnna_ctx* ctx, uint64_t* keys, uint64_t m, uint32_t n, uint64_t* row_ptr, uint32_t* col,
+                       bool dedup) {
     cudaStream_t s = ctx->stream;
     const int end_bit = 32 + bits_for(n ? n - 1 : 0);
     sort_keys_u64(ctx, keys, m, end_bit);
     uint64_t nnz = 0;
-    if (m) {
+    if (m && !dedup) {
+        nnz = m;
+        k_row_ptr_bsearch<<<grid_for((uint64_t)n + 1, 256), 256, 0, s>>>(keys, m, n, row_ptr);
+        launched(ctx, "k_row_ptr_bsearch");
+        if (col) {
+            k_low_words<<<grid_for(m, 256), 256, 0, s>>>(keys, m, col);
+            launched(ctx, "k_low_words");
+        }
+    } else if (m) {
         DevBuf<uint8_t> keep(m, s);
         k_unique_flags<<<grid_for(m, 256), 256, 0, s>>>(keys, m, keep.get());
         launched(ctx, "k_unique_flags");
@@ -191,7 +200,7 @@ gnna_status gnna_to_csr(gnna_ctx* ctx, uint32_t n, const uint32_t* d_edges, uint
             rp_tmp = DevBuf<uint64_t>((uint64_t)n + 1, s);
             rp = rp_tmp.get();
         }
-        *nnz = gnna::csr_from_keys(ctx, keys.get(), m, n, rp, d_col);
+        *nnz = gnna::csr_from_keys(ctx, keys.get(), m, n, rp, d_col, true);
         GNNA_CUDA(cudaStreamSynchronize(s));
     });
 }
@@ -208,7 +217,7 @@ gnna_status gnna_csr_transpose(gnna_ctx* ctx, const uint64_t* d_row_ptr, const u
             k_transpose_keys<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, s>>>(d_row_ptr, d_col, n, keys.get());
             gnna::launched(ctx, "k_transpose_keys");
         }
-        const uint64_t got = gnna::csr_from_keys(ctx, keys.get(), m, n, d_t_ptr, d_t_col);
+        const uint64_t got = gnna::csr_from_keys(ctx, keys.get(), m, n, d_t_ptr, d_t_col, true);
         if (got != m) gnna::raise(GNNA_ERR_DOMAIN, "csr_transpose: input rows have duplicate columns");
         GNNA_CUDA(cudaStreamSynchronize(s));
     });

@@ -1,1 +1,263 @@
+// GNN layer entry points (engine.cpp:313-408) and their backward passes.
+//
+// Forward (F64 bitwise equal to the reference; F32 the same operation order
+// in fp32):
+//   gcn_layer: norm[v] = 1/sqrt(max(deg'(v),1)) (engine.cpp:340-353);
+//              w.dim < x.dim ? normalized_aggregate(x·W) : normalized_aggregate(x)·W
+//              (engine.cpp:379-381)
+//   gin_layer: relu(((1+eps)x + sum_N x)·W + b) (engine.cpp:384-408)
+// The aggregation steps run K4 (CSR-order rows; exact per-edge
+// norm[v]*norm[u] weights), the update runs K6.
+//
+// Backward (no reference function exists: SPEC.md:9 puts autograd out of
+// scope; added in the same style, pinned in tests by finite differences of
+// the reference forward and by torch autograd in float64):
+//   GCN update-first:    dH = Â^T dY, dW = X^T dH, dX = dH W^T
+//   GCN aggregate-first: dZ = dY W^T, dW = (ÂX)^T dY, dX = Â^T dZ
+//   GIN: dU = dY ⊙ [XW+b > 0], db = Σ dU, dW = Z^T dU, dZ = dU W^T,
+//        dX = A^T dZ + (1+eps) dZ, deps = Σ X ⊙ dZ
+// Â^T is evaluated on the transposed CSR (d_rt_*) with the forward norms;
+// for the symmetric graphs to_csr(.., true) builds it is the CSR itself.
+#include <algorithm>
+#include <vector>
+
 #include "gnna_common.cuh"
+
+namespace gnna {
+void aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* row_ptr, const uint32_t* col, uint32_t r0,
+                    uint32_t rows, uint32_t dim, const void* x, void* y, int mode, const double* norm,
+                    const uint8_t* self, double alpha, uint32_t epi, const float* scale);
+void gemm(gnna_ctx* ctx, int dtype, const void* a, uint32_t m, uint32_t k, const void* w, uint32_t n,
+          const void* bias, int epilogue, const double* row_scale, void* out);
+void gemm_tn(gnna_ctx* ctx, int dtype, const void* a, const void* b, uint32_t m, uint32_t p, uint32_t q, void* out);
+void transpose(gnna_ctx* ctx, int dtype, const void* w, uint32_t rows, uint32_t cols, void* wt);
+void colsum(gnna_ctx* ctx, int dtype, const void* b, uint32_t m, uint32_t q, void* out);
+}  // namespace gnna
+
+namespace {
+
+using gnna::DevBuf;
+
+// engine.cpp:333-353: implicit self loop iff requested and v has none
+// (binary search of the sorted row), degree 0 -> 1, norm = 1/sqrt(deg).
+__global__ void k5_gcn_norm(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t n,
+                            int add_self, double* __restrict__ norm, uint8_t* __restrict__ self) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = row_ptr[v], e = row_ptr[v + 1];
+        uint64_t deg = e - b;
+        uint8_t imp = 0;
+        if (add_self) {
+            uint64_t lo = b, hi = e;
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                if (col[mid] < v) lo = mid + 1; else hi = mid;
+            }
+            if (!(lo < e && col[lo] == v)) {
+                imp = 1;
+                ++deg;
+            }
+        }
+        if (deg == 0) deg = 1;
+        norm[v] = 1.0 / sqrt((double)deg);
+        if (self) self[v] = imp;
+    }
+}
+
+template <class T>
+__global__ void k_relu_mask(const T* __restrict__ u, const T* __restrict__ b, const T* __restrict__ dy, uint64_t m,
+                            uint32_t q, T* __restrict__ du) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m * q; i += (uint64_t)gridDim.x * blockDim.x) {
+        const T v = u[i] + b[i % q];
+        du[i] = v > T(0) ? dy[i] : T(0);
+    }
+}
+
+template <class T>
+__global__ void k_dot_partial(const T* __restrict__ a, const T* __restrict__ b, uint64_t count, uint64_t per,
+                              double* __restrict__ part) {
+    __shared__ double sh[32];
+    const uint64_t s = blockIdx.x * per, e = s + per < count ? s + per : count;
+    double acc = 0.0;
+    for (uint64_t i = s + threadIdx.x; i < e; i += blockDim.x) acc += (double)a[i] * (double)b[i];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (unsigned w = 0; w < blockDim.x / 32; ++w) t += sh[w];
+        part[blockIdx.x] = t;
+    }
+}
+
+size_t esize(int dtype) {
+    if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+    return dtype == GNNA_F32 ? 4 : 8;
+}
+
+void check_dims(uint32_t in_dim, uint32_t out_dim) {
+    if (in_dim == 0 || out_dim == 0) gnna::raise(GNNA_ERR_DOMAIN, "feature dims must be positive");
+}
+
+void gcn_norm(gnna_ctx* ctx, const uint64_t* rp, const uint32_t* col, uint32_t n, int add_self, double* norm,
+              uint8_t* self) {
+    if (!n) return;
+    k5_gcn_norm<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(rp, col, n, add_self, norm, self);
+    gnna::launched(ctx, "k5_gcn_norm");
+}
+
+void normalized(gnna_ctx* ctx, int dtype, const uint64_t* rp, const uint32_t* col, uint32_t n, uint32_t dim,
+                const double* norm, const uint8_t* self, const void* x, void* y) {
+    gnna::aggregate_rows(ctx, dtype, rp, col, 0, n, dim, x, y, 1, norm, self, 0.0, 0, nullptr);
+}
+
+double dot(gnna_ctx* ctx, int dtype, const void* a, const void* b, uint64_t count) {
+    if (!count) return 0.0;
+    const unsigned grid = (unsigned)std::min<uint64_t>(4 * ctx->num_sms, (count + 1023) / 1024);
+    const uint64_t per = (count + grid - 1) / grid;
+    DevBuf<double> part(grid, ctx->stream);
+    if (dtype == GNNA_F32)
+        k_dot_partial<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(a),
+                                                            static_cast<const float*>(b), count, per, part.get());
+    else
+        k_dot_partial<double><<<grid, 256, 0, ctx->stream>>>(static_cast<const double*>(a),
+                                                             static_cast<const double*>(b), count, per, part.get());
+    gnna::launched(ctx, "k_dot_partial");
+    std::vector<double> h(grid);
+    gnna::to_host(ctx, h.data(), part.get(), grid);
+    double s = 0.0;
+    for (double v : h) s += v;
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                          int add_self_loops, double* d_norm, uint8_t* d_self) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, d_norm, d_self);
+    });
+}
+
+gnna_status gnna_normalized_aggregate(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                                      uint32_t n, uint32_t dim, const double* d_norm, const uint8_t* d_self,
+                                      const void* d_x, void* d_y) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        esize(dtype);
+        if (!d_norm) gnna::raise(GNNA_ERR_DOMAIN, "normalized_aggregate: null norm");
+        normalized(ctx, dtype, d_row_ptr, d_col, n, dim, d_norm, d_self, d_x, d_y);
+    });
+}
+
+gnna_status gnna_gcn_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                             const void* d_x, uint32_t in_dim, const void* d_w, uint32_t out_dim,
+                             int add_self_loops, void* d_y) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        const size_t es = esize(dtype);
+        check_dims(in_dim, out_dim);
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> norm(n ? n : 1, s);
+        DevBuf<uint8_t> self(n ? n : 1, s);
+        gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, norm.get(), self.get());
+        if (out_dim < in_dim) {  // engine.cpp:379-380: update first
+            DevBuf<uint8_t> t((size_t)n * out_dim * es + 1, s);
+            gnna::gemm(ctx, dtype, d_x, n, in_dim, d_w, out_dim, nullptr, 0, nullptr, t.get());
+            normalized(ctx, dtype, d_row_ptr, d_col, n, out_dim, norm.get(), self.get(), t.get(), d_y);
+        } else {  // engine.cpp:381: aggregate first
+            DevBuf<uint8_t> z((size_t)n * in_dim * es + 1, s);
+            normalized(ctx, dtype, d_row_ptr, d_col, n, in_dim, norm.get(), self.get(), d_x, z.get());
+            gnna::gemm(ctx, dtype, z.get(), n, in_dim, d_w, out_dim, nullptr, 0, nullptr, d_y);
+        }
+    });
+}
+
+gnna_status gnna_gin_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                             const void* d_x, uint32_t in_dim, double eps, const void* d_w, uint32_t out_dim,
+                             const void* d_b, void* d_y) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        const size_t es = esize(dtype);
+        check_dims(in_dim, out_dim);
+        if (!d_b) gnna::raise(GNNA_ERR_DOMAIN, "gin: null bias");
+        DevBuf<uint8_t> z((size_t)n * in_dim * es + 1, ctx->stream);
+        // engine.cpp:394-400: z = sum_N x (CSR order), then z += (1+eps) x
+        gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, in_dim, d_x, z.get(), 2, nullptr, nullptr, 1.0 + eps,
+                             0, nullptr);
+        // engine.cpp:401-406: h = z·W, relu(h + b)
+        gnna::gemm(ctx, dtype, z.get(), n, in_dim, d_w, out_dim, d_b, 1, nullptr, d_y);
+    });
+}
+
+gnna_status gnna_gcn_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                              const uint64_t* d_rt_ptr, const uint32_t* d_rt_col, uint32_t n, const void* d_x,
+                              uint32_t in_dim, const void* d_w, uint32_t out_dim, int add_self_loops, const void* d_dy,
+                              void* d_dx, void* d_dw) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        const size_t es = esize(dtype);
+        check_dims(in_dim, out_dim);
+        if (!d_rt_ptr || !d_rt_col) gnna::raise(GNNA_ERR_DOMAIN, "gcn_backward: null transposed CSR");
+        cudaStream_t s = ctx->stream;
+        DevBuf<double> norm(n ? n : 1, s);
+        DevBuf<uint8_t> self(n ? n : 1, s);
+        gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, norm.get(), self.get());
+        DevBuf<uint8_t> wt((size_t)in_dim * out_dim * es, s);
+        gnna::transpose(ctx, dtype, d_w, in_dim, out_dim, wt.get());  // out x in
+        if (out_dim < in_dim) {
+            DevBuf<uint8_t> dh((size_t)n * out_dim * es + 1, s);
+            normalized(ctx, dtype, d_rt_ptr, d_rt_col, n, out_dim, norm.get(), self.get(), d_dy, dh.get());
+            gnna::gemm_tn(ctx, dtype, d_x, dh.get(), n, in_dim, out_dim, d_dw);
+            gnna::gemm(ctx, dtype, dh.get(), n, out_dim, wt.get(), in_dim, nullptr, 0, nullptr, d_dx);
+        } else {
+            DevBuf<uint8_t> z((size_t)n * in_dim * es + 1, s), dz((size_t)n * in_dim * es + 1, s);
+            normalized(ctx, dtype, d_row_ptr, d_col, n, in_dim, norm.get(), self.get(), d_x, z.get());
+            gnna::gemm_tn(ctx, dtype, z.get(), d_dy, n, in_dim, out_dim, d_dw);
+            gnna::gemm(ctx, dtype, d_dy, n, out_dim, wt.get(), in_dim, nullptr, 0, nullptr, dz.get());
+            normalized(ctx, dtype, d_rt_ptr, d_rt_col, n, in_dim, norm.get(), self.get(), dz.get(), d_dx);
+        }
+    });
+}
+
+gnna_status gnna_gin_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                              const uint64_t* d_rt_ptr, const uint32_t* d_rt_col, uint32_t n, const void* d_x,
+                              uint32_t in_dim, double eps, const void* d_w, uint32_t out_dim, const void* d_b,
+                              const void* d_dy, void* d_dx, void* d_dw, void* d_db, double* deps) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        const size_t es = esize(dtype);
+        check_dims(in_dim, out_dim);
+        if (!d_rt_ptr || !d_rt_col) gnna::raise(GNNA_ERR_DOMAIN, "gin_backward: null transposed CSR");
+        cudaStream_t s = ctx->stream;
+        const size_t nz = (size_t)n * in_dim * es + 1, nu = (size_t)n * out_dim * es + 1;
+        DevBuf<uint8_t> z(nz, s), u(nu, s), du(nu, s), dz(nz, s), wt((size_t)in_dim * out_dim * es, s);
+        gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, in_dim, d_x, z.get(), 2, nullptr, nullptr, 1.0 + eps,
+                             0, nullptr);
+        gnna::gemm(ctx, dtype, z.get(), n, in_dim, d_w, out_dim, nullptr, 0, nullptr, u.get());
+        const uint64_t mq = (uint64_t)n * out_dim;
+        if (mq) {
+            if (dtype == GNNA_F32)
+                k_relu_mask<float><<<gnna::grid_for(mq, 256), 256, 0, s>>>(
+                    reinterpret_cast<const float*>(u.get()), static_cast<const float*>(d_b),
+                    static_cast<const float*>(d_dy), n, out_dim, reinterpret_cast<float*>(du.get()));
+            else
+                k_relu_mask<double><<<gnna::grid_for(mq, 256), 256, 0, s>>>(
+                    reinterpret_cast<const double*>(u.get()), static_cast<const double*>(d_b),
+                    static_cast<const double*>(d_dy), n, out_dim, reinterpret_cast<double*>(du.get()));
+            gnna::launched(ctx, "k_relu_mask");
+        }
+        gnna::colsum(ctx, dtype, du.get(), n, out_dim, d_db);
+        gnna::gemm_tn(ctx, dtype, z.get(), du.get(), n, in_dim, out_dim, d_dw);
+        gnna::transpose(ctx, dtype, d_w, in_dim, out_dim, wt.get());
+        gnna::gemm(ctx, dtype, du.get(), n, out_dim, wt.get(), in_dim, nullptr, 0, nullptr, dz.get());
+        // dX = A^T dZ + (1+eps) dZ: K4 mode 2 over the transposed CSR
+        gnna::aggregate_rows(ctx, dtype, d_rt_ptr, d_rt_col, 0, n, in_dim, dz.get(), d_dx, 2, nullptr, nullptr,
+                             1.0 + eps, 0, nullptr);
+        if (deps) *deps = dot(ctx, dtype, d_x, dz.get(), (uint64_t)n * in_dim);
+    });
+}
+
+}  // extern "C"

@@ -129,21 +129,5 @@ def b_alg(n_rows: int, nnz: int, dim: int, elem: int = 4) -> int:
     return 4 * nnz + elem * dim * nnz + elem * dim * n_rows + 8 * (n_rows + 1)
 
 
-def balanced_rows(row_ptr_host, parts: int):
-    """Contiguous row ranges with ~equal nnz."""
-    import numpy as np
-    rp = np.asarray(row_ptr_host)
-    n = len(rp) - 1
-    nnz = int(rp[-1])
-    cuts = [0]
-    for p in range(1, parts):
-        cuts.append(int(np.searchsorted(rp, nnz * p / parts, side="left")))
-    cuts.append(n)
-    cuts = [min(max(c, 0), n) for c in cuts]
-    for i in range(1, len(cuts)):
-        cuts[i] = max(cuts[i], cuts[i - 1])
-    return [(cuts[i], cuts[i + 1]) for i in range(parts)]
-
-
-__all__ = ["GraphConfig", "CONFIGS", "build_graph", "features", "b_alg", "balanced_rows", "scaled_config",
+__all__ = ["GraphConfig", "CONFIGS", "build_graph", "features", "b_alg", "scaled_config",
            "sample_pairs"]

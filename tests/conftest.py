@@ -58,3 +58,27 @@ def to_dev(*arrs):
             t = t.view(torch.int32)
         out.append(t.cuda())
     return out if len(out) > 1 else out[0]
+
+
+class _Golden:
+    """tests/golden/ref_golden.npz (reference-produced vectors)."""
+
+    def __init__(self, path):
+        self.z = np.load(path)
+        self.keys = set(self.z.files)
+
+    def __getitem__(self, k):
+        return self.z[k]
+
+    def ids(self, group):
+        return sorted({int(k.split("/")[1]) for k in self.keys if k.startswith(group + "/")})
+
+
+_GOLDEN = None
+
+
+def golden_cases():
+    global _GOLDEN
+    if _GOLDEN is None:
+        _GOLDEN = _Golden(os.path.join(ROOT, "tests", "golden", "ref_golden.npz"))
+    return _GOLDEN

@@ -1,0 +1,219 @@
+"""CPU (no GPU): the C-ABI library's surface, its host-side evaluator, and the
+multi-rank host logic.
+
+* libgnna.so loads and exports every entry point include/gnna.h declares;
+* without a device, gnna_create fails loudly (GNNA_ERR_CUDA) — no CPU path;
+* the performance evaluator (host C++ inside libgnna.so, decider.cpp's
+  model) equals the reference: hand goldens from test_decider.cpp, the
+  reference-produced vectors in tests/golden/, and live runs of oracle/_ref;
+* row sharding + the uneven all-gather of output rows across 2 gloo ranks.
+"""
+import ctypes as C
+import os
+import re
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_cases
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "gnna.h")).read()
+    return sorted(set(re.findall(r"GNNA_API\s+[\w\s\*]+?\b(gnna_\w+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2006_06608_b200 import capi
+    lib = capi.lib()
+    syms = header_symbols()
+    assert len(syms) > 50
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", capi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (gnna_\w+)", out))
+    assert set(syms) <= exported
+    assert lib.gnna_version().decode().startswith("gnna-b200")
+
+
+def test_no_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2006_06608_b200.capi import Context, GnnaError
+    with pytest.raises(GnnaError):
+        Context(0)
+
+
+def test_kernels_are_sm100a():
+    """The fatbin holds sm_100a SASS only (no PTX JIT path, no other arch)."""
+    from paper_2006_06608_b200 import capi
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", capi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+# ----------------------------------------------------------- evaluator
+def mi(n, e, dim, avg, sd, **kw):
+    from paper_2006_06608_b200.capi import Decider, ModelInputs
+    d = Decider()
+    m = ModelInputs.make(num_nodes=n, num_edges=e, dim=dim, avg_degree=avg, stddev_degree=sd,
+                         alpha=d.alpha_from_degrees(avg, sd))
+    for k, v in kw.items():
+        setattr(m, k, v)
+    return m
+
+
+def P(gs, dw, tpb, dim):
+    from paper_2006_06608_b200.capi import Params
+    return Params.make(ngs=gs, dw=dw, tpb=tpb, dim=dim)
+
+
+def test_decider_hand_goldens():
+    from paper_2006_06608_b200.capi import Decider, DomainError
+    d = Decider()
+    # test_decider.cpp:91-104 Eq. 6
+    assert d.select_dw(64, 32) == 32 and d.select_dw(16, 32) == 16 and d.select_dw(8, 16) == 8
+    with pytest.raises(DomainError):
+        d.select_dw(16, 3)
+    # test_decider.cpp:106-124 select_ngs
+    roomy = mi(1000, 10000, 16, 1000.0, 0.0)
+    assert d.select_ngs(16, 128, roomy) == 1024
+    roomy.dim = 100
+    assert d.select_ngs(32, 128, roomy) == 328
+    assert d.select_ngs(16, 128, mi(1000, 10000, 16, 14.33, 0.0)) == 14 * 32
+    assert d.select_ngs(16, 128, mi(1000, 10, 16, 0.01, 0.0)) == 1
+    # test_decider.cpp:126-131 dp_size
+    assert d.dp_size(96 * 1024, 24.0) == pytest.approx(1.0)
+    assert d.dp_size(96 * 1024, 12.0) == pytest.approx(2.0)
+    # test_decider.cpp:133-141 latency worked example 61.7897727
+    w = mi(500, 1000, 30, 1.0, 0.0)
+    w.alpha = 0.2
+    assert d.estimate_latency(P(2, 32, 64, 30), w) == pytest.approx(30000.0 / 1408.0 * 2.9, rel=1e-12)
+    # test_decider.cpp:166-173 alpha map
+    assert d.alpha_from_degrees(10.0, 10.0) == pytest.approx(0.225)
+    assert d.alpha_from_degrees(10.0, 50.0) == pytest.approx(0.30)
+    # test_decider.cpp:229-245 auto_params goldens
+    p = d.auto_params(mi(500, 1000, 16, 2.0, 0.0))
+    assert (p.dim, p.dw, p.tpb, p.ngs) == (16, 16, 128, 64)
+    p = d.auto_params(mi(100000, 1000000, 16384, 10.0, 0.0))
+    assert (p.dw, p.tpb, p.ngs) == (32, 32, 2)
+    # test_decider.cpp:187-189 defaults
+    m = mi(9, 16, 64, 1.0, 0.0)
+    assert (m.max_tpb, m.smem_per_block, m.capability) == (1024, 96 * 1024, 4096)
+
+
+def test_decider_against_reference_goldens():
+    from paper_2006_06608_b200.capi import Decider, ModelInputs
+    d = Decider()
+    g = golden_cases()
+    for i in g.ids("dec"):
+        n, e, dim = (int(v) for v in g[f"dec/{i}/inputs"])
+        avg, sd, alpha = (float(v) for v in g[f"dec/{i}/fin"])
+        assert d.alpha_from_degrees(avg, sd) == alpha
+        m = ModelInputs.make(num_nodes=n, num_edges=e, dim=dim, avg_degree=avg, stddev_degree=sd, alpha=alpha)
+        assert d.auto_params(m).tolist() == g[f"dec/{i}/auto"].tolist()
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libgnnsim_ref.so")),
+                    reason="oracle/_ref not built")
+def test_decider_against_live_reference(ref):
+    from oracle.cpu import model_inputs
+    from paper_2006_06608_b200.capi import Decider, ModelInputs
+    d = Decider()
+    rng = np.random.default_rng(3)
+    for t in range(60):
+        n = int(rng.integers(1, 10 ** 6))
+        e = int(rng.integers(1, 10 ** 7))
+        dim = int(rng.choice([1, 3, 16, 30, 64, 100, 128, 602, 16384]))
+        avg = float(rng.choice([0.0, 0.01, 1.0, 2.0, 12.0, 14.33, 1000.0]))
+        sd = float(rng.random() * 3 * max(avg, 1))
+        r = model_inputs(n, e, dim, avg, sd, alpha=ref.alpha_from_degrees(avg, sd))
+        m = ModelInputs.make(num_nodes=n, num_edges=e, dim=dim, avg_degree=avg, stddev_degree=sd,
+                             alpha=d.alpha_from_degrees(avg, sd))
+        assert m.alpha == r.alpha
+        if t % 5 == 0:
+            m.smem_per_block = r.smem_per_block = int(rng.choice([100, 4096, 96 * 1024]))
+        assert d.auto_params(m).tolist() == ref.auto_params(r).tolist()
+        for gs, dw, tpb in ((1, 32, 32), (16, 16, 128), (64, 8, 256), (3, 7, 96)):
+            p = P(gs, dw, tpb, dim)
+            pr = np.array(p.tolist(), np.uint32)
+            if n and e:
+                assert d.estimate_latency(p, m) == ref.estimate_latency(pr, r)
+            assert d.feasible(p, m) == ref.feasible(pr, r)
+        if t % 6 == 0 and n and e and avg > 0:
+            seed = int(rng.integers(0, 1000))
+            b1, l1, f1, tr1 = d.search_params(m, 8, 16, seed)
+            b2, l2, f2, tr2 = ref.search_params(r, 8, 16, seed)
+            assert b1.tolist() == b2.tolist() and l1 == l2 and f1 == f2 and np.array_equal(tr1, tr2)
+
+
+# ------------------------------------------------------- multi-rank logic
+def test_row_ranges_balance():
+    from paper_2006_06608_b200.shard import row_ranges
+    rng = np.random.default_rng(1)
+    deg = rng.zipf(2.0, size=5000).clip(0, 3000)
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    for parts in (1, 2, 3, 4, 8):
+        rr = row_ranges(rp, parts)
+        assert rr[0][0] == 0 and rr[-1][1] == 5000
+        assert all(rr[i][1] == rr[i + 1][0] for i in range(parts - 1))
+        loads = [int(rp[b] - rp[a]) for a, b in rr]
+        assert max(loads) <= rp[-1] / parts + deg.max() + 1
+    empty = row_ranges(np.array([0, 0, 0], np.uint64), 4)  # no edges: ranges still tile the rows
+    assert empty[0][0] == 0 and empty[-1][1] == 2 and all(empty[i][1] == empty[i + 1][0] for i in range(3))
+
+
+_WORKER = r'''
+import os, sys
+sys.path.insert(0, os.environ["GNNA_ROOT"])
+import numpy as np, torch, torch.distributed as dist
+from oracle.cpu import Oracle
+from paper_2006_06608_b200.shard import row_ranges, allgather_rows
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+orc = Oracle("orc")
+rng = np.random.default_rng(7)
+n = 700
+w = 1.0 / np.arange(1, n + 1)
+src = rng.choice(n, size=6000, p=w / w.sum())
+edges = np.stack([src, rng.integers(0, n, 6000)], 1).astype(np.uint32)
+rp, col = orc.to_csr(n, edges, True)
+x = rng.random((n, 8))
+full = orc.aggregate_oracle(rp, col, x)
+ranges = row_ranges(rp, world)
+a, b = ranges[rank]
+y = torch.zeros((n, 8), dtype=torch.float64)
+# this rank's rows: the row-slice subgraph is a rows x n CSR over the full x
+sub_rp = (rp[a:b + 1] - rp[a]).astype(np.uint64)
+sub_col = col[rp[a]:rp[b]]
+if b > a:
+    y[a:b] = torch.from_numpy(orc.aggregate_oracle(np.concatenate([sub_rp, np.full(n - (b - a), sub_rp[-1], np.uint64)]), sub_col, x)[: b - a])
+allgather_rows(y, ranges, rank)
+assert np.array_equal(y.numpy(), full), "all-gathered rows differ"
+dist.barrier()
+print("rank", rank, "ok", ranges[rank])
+'''
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_row_sharded_allgather_gloo_world2(tmp_path):
+    script = tmp_path / "worker.py"
+    script.write_text(_WORKER)
+    env = dict(os.environ, GNNA_ROOT=ROOT, OMP_NUM_THREADS="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2", "--master-addr",
+                        "127.0.0.1", "--master-port", str(_free_port()), str(script)], capture_output=True, text=True,
+                       env=env, timeout=240)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert r.stdout.count(" ok ") == 2
