@@ -84,6 +84,14 @@ GNNA_API const char* gnna_version(void);
 /* Number of kernels this library has launched on ctx (for bench.py). */
 GNNA_API uint64_t gnna_launch_count(const gnna_ctx* ctx);
 
+/* Device memory for hosts that do not link the CUDA runtime themselves (the
+ * gnnsim:: C++ drop-in).  Allocation is stream-ordered on ctx's stream;
+ * gnna_copy_to_host synchronises the stream before returning. */
+GNNA_API gnna_status gnna_device_alloc(gnna_ctx* ctx, size_t bytes, void** out);
+GNNA_API gnna_status gnna_device_free(gnna_ctx* ctx, void* p);
+GNNA_API gnna_status gnna_copy_to_device(gnna_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);
+GNNA_API gnna_status gnna_copy_to_host(gnna_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
+
 /* -------------------------------------------------- parameter domain --- */
 /* schedule.cpp:7-14 KernelParams::validate — same order, same messages. */
 GNNA_API gnna_status gnna_validate_params(gnna_ctx* ctx, const gnna_params* p);
@@ -142,6 +150,16 @@ GNNA_API gnna_status gnna_cost_report(gnna_ctx* ctx, const gnna_plan* plan, int 
 GNNA_API gnna_status gnna_simulate_cache(gnna_ctx* ctx, const gnna_plan* plan, uint64_t cache_capacity,
                                 uint64_t cache_line, uint32_t dim, uint64_t* hits,
                                 uint64_t* accesses);
+
+/* engine.hpp:77 simulate_cache over an explicit warp schedule (WarpSchedule:
+ * warp w covers col[d_begin[w] .. d_end[w]), blocks of warps_per_block
+ * consecutive warps).  Same replay as gnna_simulate_cache; used by the C++
+ * drop-in, whose callers may hand in any schedule. */
+GNNA_API gnna_status gnna_simulate_cache_ranges(gnna_ctx* ctx, const uint32_t* d_col,
+                                       const uint64_t* d_begin, const uint64_t* d_end,
+                                       uint64_t num_warps, uint32_t warps_per_block,
+                                       uint64_t cache_capacity, uint64_t cache_line,
+                                       uint32_t dim, uint64_t* hits, uint64_t* accesses);
 
 /* engine.hpp:66 aggregate_oracle: y[v] = sum in CSR order (K4). */
 GNNA_API gnna_status gnna_aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
@@ -260,6 +278,8 @@ GNNA_API gnna_status gnna_apply_mapping_edges(gnna_ctx* ctx, const uint32_t* d_e
 /* decider.hpp:46-94, the reference's model with its defaults. */
 GNNA_API gnna_status gnna_model_inputs_from_graph(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
                                          uint32_t dim, gnna_model_inputs* out);
+/* Message of the last evaluator DomainError on this thread (decider.cpp's text). */
+GNNA_API const char* gnna_decider_last_error(void);
 GNNA_API double gnna_alpha_from_degrees(double avg_degree, double stddev_degree);
 GNNA_API gnna_status gnna_select_dw(uint32_t dim, uint32_t tpw, uint32_t* out);
 GNNA_API gnna_status gnna_select_ngs(uint32_t dw, uint32_t tpb, const gnna_model_inputs* in,

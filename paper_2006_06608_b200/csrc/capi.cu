@@ -60,6 +60,37 @@ const char* gnna_last_error(const gnna_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 uint64_t gnna_launch_count(const gnna_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+gnna_status gnna_device_alloc(gnna_ctx* ctx, size_t bytes, void** out) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (!out) gnna::raise(GNNA_ERR_DOMAIN, "null output pointer");
+        *out = nullptr;
+        GNNA_CUDA(cudaMallocAsync(out, bytes ? bytes : 1, ctx->stream));
+    });
+}
+
+gnna_status gnna_device_free(gnna_ctx* ctx, void* p) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (p) GNNA_CUDA(cudaFreeAsync(p, ctx->stream));
+    });
+}
+
+gnna_status gnna_copy_to_device(gnna_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (bytes) GNNA_CUDA(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    });
+}
+
+gnna_status gnna_copy_to_host(gnna_ctx* ctx, void* h_dst, const void* d_src, size_t bytes) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (bytes) GNNA_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        GNNA_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const uint64_t* h_row_ptr, const uint32_t* h_col,
                                      uint32_t n, uint32_t row_begin, uint32_t row_end, const gnna_params* p,
                                      int strategy, int dim_mode, const void* h_x, void* h_y, uint64_t line_bytes,

@@ -108,7 +108,8 @@ __global__ void k8_count(CountArgs a, unsigned long long* __restrict__ out) {
 
 // ---------------------------------------------------------- LRU replay ---
 struct ReplayArgs {
-    const uint64_t* part_ptr;
+    const uint64_t* begin;  // per warp CSR range [begin[w], end[w])
+    const uint64_t* end;
     const uint32_t* col;
     uint64_t G;
     uint32_t wpb;
@@ -129,10 +130,9 @@ __global__ void k8_block_access(ReplayArgs a, unsigned long long* __restrict__ m
     const uint32_t lane = threadIdx.x & 31;
     for (uint64_t sb = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; sb < nblk;
          sb += (uint64_t)gridDim.x * (blockDim.x / 32)) {
-        const uint64_t lo = a.part_ptr[sb * a.wpb];
-        const uint64_t hi = a.part_ptr[umin64((sb + 1) * a.wpb, a.G)];
         uint64_t acc = 0;
-        for (uint64_t p = lo + lane; p < hi; p += 32) acc += nlines(a.col[p], a);
+        for (uint64_t w = sb * a.wpb; w < umin64((sb + 1) * a.wpb, a.G); ++w)
+            for (uint64_t p = a.begin[w] + lane; p < a.end[w]; p += 32) acc += nlines(a.col[p], a);
         acc = warp_sum(acc);
         if (lane == 0) atomicMax(maxacc, (unsigned long long)acc);
     }
@@ -161,8 +161,8 @@ __global__ void k8_replay(ReplayArgs a, uint64_t* __restrict__ gkeys, uint32_t* 
         const uint32_t nw = (uint32_t)umin64(a.wpb, a.G - u0);
         uint64_t myb = 0, mysz = 0;
         if (lane < nw) {
-            myb = a.part_ptr[u0 + lane];
-            mysz = a.part_ptr[u0 + lane + 1] - myb;
+            myb = a.begin[u0 + lane];
+            mysz = a.end[u0 + lane] - myb;
         }
         uint64_t maxsz = mysz;
         for (int o = 16; o; o >>= 1) maxsz = max(maxsz, __shfl_xor_sync(0xffffffffu, maxsz, o));
@@ -229,16 +229,17 @@ void cache_validate(uint64_t cap, uint64_t line) {
         gnna::raise(GNNA_ERR_DOMAIN, "cache capacity must be a positive multiple of the line size");
 }
 
-void replay(gnna_ctx* ctx, const gnna_plan* plan, uint64_t cap_bytes, uint64_t line, uint32_t dim, uint64_t* hits,
-            uint64_t* accesses) {
+void replay_ranges(gnna_ctx* ctx, const uint64_t* begin, const uint64_t* end, const uint32_t* col, uint64_t G,
+                   uint32_t wpb, uint64_t cap_bytes, uint64_t line, uint32_t dim, uint64_t* hits, uint64_t* accesses) {
     cudaStream_t s = ctx->stream;
     *hits = *accesses = 0;
-    if (plan->G == 0) return;
+    if (G == 0) return;
     ReplayArgs a{};
-    a.part_ptr = plan->part_ptr.get();
-    a.col = plan->col;
-    a.G = plan->G;
-    a.wpb = plan->wpb_params;
+    a.begin = begin;
+    a.end = end;
+    a.col = col;
+    a.G = G;
+    a.wpb = wpb;
     a.row_bytes = (uint64_t)dim * 4;
     a.line = line;
     a.cap = cap_bytes / line;
@@ -273,6 +274,12 @@ void replay(gnna_ctx* ctx, const gnna_plan* plan, uint64_t cap_bytes, uint64_t l
     gnna::to_host(ctx, r, out.get(), 2);
     *hits = r[0];
     *accesses = r[1];
+}
+
+void replay(gnna_ctx* ctx, const gnna_plan* plan, uint64_t cap_bytes, uint64_t line, uint32_t dim, uint64_t* hits,
+            uint64_t* accesses) {
+    replay_ranges(ctx, plan->part_ptr.get(), plan->part_ptr.get() + 1, plan->col, plan->G, plan->wpb_params, cap_bytes,
+                  line, dim, hits, accesses);
 }
 
 }  // namespace
@@ -348,6 +355,20 @@ gnna_status gnna_simulate_cache(gnna_ctx* ctx, const gnna_plan* plan, uint64_t c
         cache_validate(cache_capacity, cache_line);
         if (dim == 0) gnna::raise(GNNA_ERR_DOMAIN, "dim must be positive");
         replay(ctx, plan, cache_capacity, cache_line, dim, hits, accesses);
+    });
+}
+
+gnna_status gnna_simulate_cache_ranges(gnna_ctx* ctx, const uint32_t* d_col, const uint64_t* d_begin,
+                                       const uint64_t* d_end, uint64_t num_warps, uint32_t warps_per_block,
+                                       uint64_t cache_capacity, uint64_t cache_line, uint32_t dim, uint64_t* hits,
+                                       uint64_t* accesses) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        cache_validate(cache_capacity, cache_line);
+        if (dim == 0) gnna::raise(GNNA_ERR_DOMAIN, "dim must be positive");
+        if (warps_per_block < 1 || warps_per_block > 32) gnna::raise(GNNA_ERR_DOMAIN, "warps per block must be in [1, 32]");
+        replay_ranges(ctx, d_begin, d_end, d_col, num_warps, warps_per_block, cache_capacity, cache_line, dim, hits,
+                      accesses);
     });
 }
 
