@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgnna.so")
+LIB_PATH = os.environ.get("GNNA_LIB") or os.path.join(HERE, "libgnna.so")  # GNNA_LIB: experiment builds
 
 OK, ERR_DOMAIN, ERR_INTERNAL, ERR_CUDA, ERR_OOM = 0, 1, 2, 3, 4
 NAIVE_ATOMIC, UNIT_SYNC, WARP_SHARED = 0, 1, 2

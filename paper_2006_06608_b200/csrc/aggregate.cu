@@ -21,6 +21,7 @@
 // engine.cpp:149-160), with exact fp64 variants of normalized_aggregate
 // (engine.cpp:355-367) and the GIN self term (engine.cpp:394-400).
 #include <algorithm>
+#include <cstdlib>
 
 #include "gnna_common.cuh"
 
@@ -183,9 +184,78 @@ __device__ __forceinline__ void gather(const AggArgs& a, uint64_t b, uint64_t e,
     }
 }
 
+// Occupancy vs. loads-in-flight, measured on B200 (profiles/README.md, r01
+// A/B): register-capped occupancy beats deep unrolling.  Wide teams (d >= 32
+// fp32) run 6 row vectors in flight per lane at <= 64 registers (4 CTAs of
+// 256 threads per SM); narrow teams (d = 16) hold 32/TEAM indices per lane,
+// so they run 8 in flight at <= 80 registers (3 CTAs).  GNNA_K3_UNR /
+// GNNA_K3_MINB override both for experiment builds (`make variants`).
+template <int TEAM, int KMAX>
+struct K3Tune {
+#ifdef GNNA_K3_UNR
+    static constexpr int unr1 = GNNA_K3_UNR;
+#else
+    static constexpr int unr1 = TEAM >= 8 ? 6 : 8;
+#endif
+#ifdef GNNA_K3_MINB
+    static constexpr int minb = GNNA_K3_MINB;
+#else
+    static constexpr int minb = TEAM >= 8 ? 4 : 3;
+#endif
+    static constexpr int unr = KMAX == 1 ? unr1 : (KMAX == 2 ? (unr1 + 1) / 2 : (unr1 + 3) / 4);
+};
+
+// Team-cooperative gather over [b, e) into acc, same per-lane summation
+// order as `gather` (CSR order from 0).  The warp walks its teams' neighbour
+// lists in batches of 32 CSR entries: one coalesced index load per batch
+// (each lane holds 32/TEAM indices), indices are broadcast inside the team
+// with width-TEAM shuffles, and UNR x KMAX 16-byte row vectors per lane are
+// in flight before the in-order adds.  Loop bounds are warp-uniform (max
+// over the warp's teams), loads/adds of finished teams are predicated off.
+template <class T, int VEC, int TEAM, int KMAX>
+__device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64_t e, uint32_t lane,
+                                            const uint32_t (&off)[KMAX], const bool (&ok)[KMAX],
+                                            Vec<T, VEC> (&acc)[KMAX]) {
+    constexpr int UNR = K3Tune<TEAM, KMAX>::unr;
+    constexpr int R = 32 / TEAM;  // indices held per lane per batch
+    const T* __restrict__ x = static_cast<const T*>(a.x);
+    const uint32_t* __restrict__ col = a.col;
+    const uint32_t len = (uint32_t)(e - b);
+    const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
+    for (uint32_t base = 0; base < wlen; base += 32) {
+        uint32_t idxr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t j = base + lane + r * TEAM;
+            idxr[r] = j < len ? __ldg(col + b + j) : 0u;
+        }
+        const uint32_t cnt = len > base ? min(32u, len - base) : 0u;
+        const uint32_t wcnt = __reduce_max_sync(0xffffffffu, cnt);
+#pragma unroll
+        for (int q0 = 0; q0 < 32; q0 += UNR) {
+            if ((uint32_t)q0 >= wcnt) break;
+            uint32_t idx[UNR];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) idx[u] = __shfl_sync(0xffffffffu, idxr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
+            Vec<T, VEC> val[UNR][KMAX];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (ok[k] && (uint32_t)(q0 + u) < cnt)
+                        val[u][k] = ldv<T, VEC>(x + (size_t)idx[u] * a.dim + off[k]);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (ok[k] && (uint32_t)(q0 + u) < cnt) vadd(acc[k], val[u][k]);
+        }
+    }
+}
+
 // ----------------------------------------------------------------- K3 ---
 template <class T, int VEC, int TEAM, int KMAX>
-__global__ void __launch_bounds__(256) k3_aggregate(AggArgs a) {
+__global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(AggArgs a) {
     using VT = Vec<T, VEC>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VT* sm = reinterpret_cast<VT*>(smem_raw);  // [upc][KMAX][TEAM]
@@ -210,7 +280,7 @@ __global__ void __launch_bounds__(256) k3_aggregate(AggArgs a) {
         VT acc[KMAX];
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) vzero(acc[k]);
-        if (active) gather<T, VEC, KMAX>(a, b, e, L.off, L.ok, acc);
+        gather_team<T, VEC, TEAM, KMAX>(a, b, e, lane, L.off, L.ok, acc);  // all lanes (b = e for idle teams)
         if (active && direct) {
 #pragma unroll
             for (int k = 0; k < KMAX; ++k)
@@ -280,13 +350,13 @@ __global__ void __launch_bounds__(256) k3b_fixup(AggArgs a, const uint32_t* __re
 // c = norm[v]*norm[u], separately rounded c*x, implicit self loop last).
 // MODE 2: exact GIN input (CSR-order sum, then + alpha*x[v]).
 template <class T, int VEC, int TEAM, int KMAX, int MODE>
-__global__ void __launch_bounds__(256) k4_rows(AggArgs a) {
+__global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k4_rows(AggArgs a) {
     using VT = Vec<T, VEC>;
     const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
     const uint64_t i = (uint64_t)blockIdx.x * (256 / TEAM) + tu;
-    if (i >= a.units) return;
-    const uint32_t v = a.r0 + (uint32_t)i;
-    const uint64_t b = __ldg(a.row_ptr + v), e = __ldg(a.row_ptr + v + 1);
+    const bool active = i < a.units;  // no early exit: gather_team is warp-collective
+    const uint32_t v = active ? a.r0 + (uint32_t)i : 0u;
+    const uint64_t b = active ? __ldg(a.row_ptr + v) : 0, e = active ? __ldg(a.row_ptr + v + 1) : 0;
     const T* __restrict__ x = static_cast<const T*>(a.x);
     for (uint32_t k0 = 0; k0 < a.kpl; k0 += KMAX) {
         Lanes<T, VEC, TEAM, KMAX> L;
@@ -303,23 +373,23 @@ __global__ void __launch_bounds__(256) k4_rows(AggArgs a) {
                 for (int k = 0; k < KMAX; ++k)
                     if (L.ok[k]) vaxpy_rn(acc[k], c, ldv<T, VEC>(x + (size_t)uu * a.dim + L.off[k]));
             }
-            if (a.self && a.self[v]) {
+            if (active && a.self && a.self[v]) {
                 const T c = T(__dmul_rn(nv, nv));
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k)
                     if (L.ok[k]) vaxpy_rn(acc[k], c, ldv<T, VEC>(x + (size_t)v * a.dim + L.off[k]));
             }
         } else {
-            gather<T, VEC, KMAX>(a, b, e, L.off, L.ok, acc);
+            gather_team<T, VEC, TEAM, KMAX>(a, b, e, lane, L.off, L.ok, acc);
             if constexpr (MODE == 2) {
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k)
-                    if (L.ok[k]) vaxpy_rn(acc[k], T(a.alpha), ldv<T, VEC>(x + (size_t)v * a.dim + L.off[k]));
+                    if (active && L.ok[k]) vaxpy_rn(acc[k], T(a.alpha), ldv<T, VEC>(x + (size_t)v * a.dim + L.off[k]));
             }
         }
 #pragma unroll
         for (int k = 0; k < KMAX; ++k)
-            if (L.ok[k]) store_final<T, VEC>(a, v, L.off[k], acc[k]);
+            if (active && L.ok[k]) store_final<T, VEC>(a, v, L.off[k], acc[k]);
     }
 }
 
@@ -347,26 +417,32 @@ Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const
     const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
     s.vec = (dim % full == 0 && aligned) ? full : 1;
     const uint32_t nvec = dim / s.vec;
-    // dw counts scalar dimension workers (schedule.hpp:16); with 16-byte
-    // lanes one vector lane stands for `vec` of them.
-    uint32_t t = pow2ceil((dw + s.vec - 1) / s.vec);
+    // The physical lane map is free: every output dimension is summed in the
+    // same order whatever lane owns it.  By default a team spans the whole
+    // row in 16-byte vectors (up to a warp); GNNA_K3_DW_TEAMS=1 restores the
+    // literal map (dw scalar dimension workers = dw/vec vector lanes).
+    static const bool dw_teams = std::getenv("GNNA_K3_DW_TEAMS") != nullptr;
+    uint32_t t = dw_teams ? pow2ceil((dw + s.vec - 1) / s.vec) : 32u;
     t = std::min<uint32_t>(t, pow2ceil(nvec));
     t = std::min<uint32_t>(t, team_cap);
     t = std::max<uint32_t>(t, 1);
     s.team = std::min<uint32_t>(t, 32);
     s.kpl = (nvec + s.team - 1) / s.team;
-    s.kmax = s.kpl <= 1 ? 1 : 4;
+    s.kmax = s.kpl <= 1 ? 1 : (s.kpl <= 2 ? 2 : 4);
     return s;
 }
 
 template <class T, int VEC, int TEAM>
 void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, const gnna_plan* plan) {
     const size_t smem = (size_t)a.upc * kmax * TEAM * sizeof(Vec<T, VEC>);
+    const unsigned threads = (a.upc * TEAM + 31) / 32 * 32;  // whole warps (gather_team is warp-collective)
     if (grid) {
         if (kmax == 1)
-            k3_aggregate<T, VEC, TEAM, 1><<<(unsigned)grid, a.upc * TEAM, smem, ctx->stream>>>(a);
+            k3_aggregate<T, VEC, TEAM, 1><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+        else if (kmax == 2)
+            k3_aggregate<T, VEC, TEAM, 2><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
         else
-            k3_aggregate<T, VEC, TEAM, 4><<<(unsigned)grid, a.upc * TEAM, smem, ctx->stream>>>(a);
+            k3_aggregate<T, VEC, TEAM, 4><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
         gnna::launched(ctx, "k3_aggregate");
     }
     const uint64_t nfix = plan->nsplit + plan->nempty;
@@ -394,6 +470,8 @@ void launch_k4_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax) {
     const unsigned grid = (unsigned)((a.units + 256 / TEAM - 1) / (256 / TEAM));
     if (kmax == 1)
         k4_rows<T, VEC, TEAM, 1, MODE><<<grid, 256, 0, ctx->stream>>>(a);
+    else if (kmax == 2)
+        k4_rows<T, VEC, TEAM, 2, MODE><<<grid, 256, 0, ctx->stream>>>(a);
     else
         k4_rows<T, VEC, TEAM, 4, MODE><<<grid, 256, 0, ctx->stream>>>(a);
     gnna::launched(ctx, "k4_rows");
