@@ -140,6 +140,26 @@ GNNA_API gnna_status gnna_plan_arrays(const gnna_plan* plan, const uint64_t** d_
  * GNNA_F32 follows the same tree in fp32.  x, y: n x dim row-major. */
 GNNA_API gnna_status gnna_aggregate(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
                            const void* d_x, void* d_y);
+/* Options of gnna_aggregate_ex: the fused forms the layer entry points need
+ * (engine.cpp:338-408).  For each output row v of the plan:
+ *   y[v] = relu?( row_scale[v] * ( sum_e edge_weight[e] * x[col[e]]
+ *                                  + self_weight[v] * x[v] ) )  (masked)
+ * edge_weight is indexed by CSR position (F32 only; NULL = all ones);
+ * self_weight NULL uses the constant alpha (0 = no self term); row_scale NULL
+ * = 1; mask (same shape/dtype as y) zeroes y where mask <= 0 (ReLU backward).
+ * dim 0 = the plan's params.dim; any other width reuses the plan's schedule. */
+typedef struct {
+    uint32_t dim;
+    const float* edge_weight;
+    const float* self_weight;
+    double alpha;
+    const float* row_scale;
+    int relu;
+    const void* mask;
+} gnna_agg_opts;
+GNNA_API gnna_status gnna_aggregate_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
+                              const void* d_x, void* d_y, const gnna_agg_opts* opts);
+
 /* engine.hpp:30-53 + engine.cpp:242-289: the integer CostReport of
  * aggregate_scheduled for this plan (K8).  cache_line == 0 disables the LRU
  * replay (EngineOptions::cache = nullopt). */
@@ -193,6 +213,13 @@ GNNA_API gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const ui
  * NULL) receives the implicit-self flags. */
 GNNA_API gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
                           uint32_t n, int add_self_loops, double* d_norm, uint8_t* d_self);
+/* fp32 operands of the fused normalized aggregation (gnna_aggregate_ex):
+ * d_row_scale[v] = norm[v], d_self_weight[v] = norm[v] if v gets an implicit
+ * self loop else 0, d_edge_weight[e] = norm[col[e]] (any may be NULL).  Then
+ * y = row_scale * (A_w x + self_weight * x) = D^-1/2 (A [+I]) D^-1/2 x. */
+GNNA_API gnna_status gnna_gcn_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                             uint32_t n, int add_self_loops, float* d_row_scale,
+                             float* d_self_weight, float* d_edge_weight);
 /* engine.cpp:338-369 normalized_aggregate, z = D^-1/2 (A [+I]) D^-1/2 x,
  * F64 bitwise as the reference.  transpose != 0 applies the adjoint
  * (out[u] += norm[v]norm[u] x[v]); it requires the transposed CSR
@@ -208,7 +235,12 @@ GNNA_API gnna_status gnna_normalized_aggregate(gnna_ctx* ctx, int dtype, const u
 GNNA_API gnna_status gnna_gemm(gnna_ctx* ctx, int dtype, const void* d_a, uint32_t m, uint32_t k,
                       const void* d_w, uint32_t n_out, const void* d_bias, int epilogue,
                       const double* d_row_scale, void* d_out);
-/* engine.hpp:93 gcn_layer / engine.hpp:108 gin_layer, forward (F64 bitwise). */
+/* Weight gradient product out (p x q) = a^T b, a: m x p, b: m x q (backward
+ * of matmul; row-chunk partials summed in chunk order: deterministic). */
+GNNA_API gnna_status gnna_gemm_tn(gnna_ctx* ctx, int dtype, const void* d_a, const void* d_b, uint32_t m,
+                         uint32_t p, uint32_t q, void* d_out);
+/* engine.hpp:93 gcn_layer / engine.hpp:108 gin_layer, forward (F64 bitwise;
+ * F32 runs a scheduled plan with the normalisation fused into K3). */
 GNNA_API gnna_status gnna_gcn_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
                              const uint32_t* d_col, uint32_t n, const void* d_x,
                              uint32_t in_dim, const void* d_w, uint32_t out_dim,

@@ -71,6 +71,12 @@ class ModelInputs(C.Structure):
                    capability, alpha)
 
 
+class AggOpts(C.Structure):
+    """gnna_agg_opts (include/gnna.h)."""
+    _fields_ = [("dim", C.c_uint32), ("edge_weight", C.c_void_p), ("self_weight", C.c_void_p), ("alpha", C.c_double),
+                ("row_scale", C.c_void_p), ("relu", C.c_int), ("mask", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -283,6 +289,16 @@ class Context:
                                          _ptr(norm), _ptr(sl)))
         return norm[:n], sl[:n]
 
+    def gcn_weights(self, row_ptr, col, self_loops=False):
+        """fp32 (row_scale[n], self_weight[n], edge_weight[nnz]) of D^-1/2 (A [+I]) D^-1/2."""
+        n = row_ptr.numel() - 1
+        torch = self.torch
+        rs, sw = self._empty(max(n, 1), torch.float32), self._empty(max(n, 1), torch.float32)
+        ew = self._empty(max(col.numel(), 1), torch.float32)
+        self._check(self.L.gnna_gcn_weights(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), C.c_int(int(self_loops)),
+                                            _ptr(rs), _ptr(sw), _ptr(ew)))
+        return rs[:n], sw[:n], ew[: col.numel()]
+
     def normalized_aggregate(self, row_ptr, col, x, norm, selfl, out=None):
         n = row_ptr.numel() - 1
         if out is None:
@@ -424,6 +440,17 @@ class Plan:
             out = self.ctx.torch.zeros_like(x)
         self.ctx._check(self.ctx.L.gnna_aggregate(self.ctx.h, self.h, C.c_int(_dtype_code(x)),
                                                   C.c_int(dim_mode), _ptr(x), _ptr(out)))
+        return out
+
+    def aggregate_ex(self, x, out=None, edge_weight=None, self_weight=None, alpha=0.0, row_scale=None, relu=False,
+                     mask=None, dim_mode=DIM_CYCLIC):
+        """gnna_aggregate_ex: y = relu?(row_scale * (A_w x + self_weight * x)) [masked]; x may be any width."""
+        if out is None:
+            out = self.ctx.torch.empty_like(x)
+        o = AggOpts(int(x.shape[1]), _ptr(edge_weight), _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu),
+                    _ptr(mask))
+        self.ctx._check(self.ctx.L.gnna_aggregate_ex(self.ctx.h, self.h, C.c_int(_dtype_code(x)), C.c_int(dim_mode),
+                                                     _ptr(x), _ptr(out), C.byref(o)))
         return out
 
     def cost(self, dim_mode=DIM_CYCLIC, line=128, cache=None):

@@ -22,6 +22,7 @@
 // (engine.cpp:355-367) and the GIN self term (engine.cpp:394-400).
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gnna_common.cuh"
 
@@ -88,7 +89,7 @@ __device__ __forceinline__ void vaxpy_rn(Vec<T, VEC>& acc, T c, const Vec<T, VEC
     for (int i = 0; i < VEC; ++i) acc.a[i] = add_rn(acc.a[i], mul_rn(c, v.a[i]));
 }
 
-enum : uint32_t { EPI_SCALE = 1, EPI_SELF = 2, EPI_RELU = 4 };
+enum : uint32_t { EPI_SCALE = 1, EPI_SELF = 2, EPI_RELU = 4, EPI_MASK = 8 };
 
 struct AggArgs {
     // schedule
@@ -109,7 +110,10 @@ struct AggArgs {
     // epilogue (final writes only)
     uint32_t epi;
     const float* scale;   // EPI_SCALE: per-row multiplier (fp32 GCN fold)
-    double alpha;         // EPI_SELF:  y += alpha * x[v]
+    double alpha;         // EPI_SELF:  y += alpha * x[v]  (or sw[v] * x[v] when sw != null)
+    const float* sw;      // EPI_SELF per-node self weights (GCN: norm[v] if v gets an implicit loop, else 0)
+    const void* mask;     // EPI_MASK: y[v][d] = mask[v][d] > 0 ? y[v][d] : 0 (ReLU backward)
+    const float* ew;      // per-edge weights in CSR order (fp32 path): acc += ew[e] * x[col[e]]
     // K4 exact modes
     const double* norm;
     const uint8_t* self;
@@ -135,8 +139,11 @@ __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32
     T* y = static_cast<T*>(a.y) + (size_t)v * a.dim + off;
     if (a.epi) {
         if (a.epi & EPI_SELF) {
-            const Vec<T, VEC> xv = ldv<T, VEC>(static_cast<const T*>(a.x) + (size_t)v * a.dim + off);
-            vaxpy_rn(val, T(a.alpha), xv);
+            const T c = a.sw ? T(a.sw[v]) : T(a.alpha);
+            if (c != T(0)) {
+                const Vec<T, VEC> xv = ldv<T, VEC>(static_cast<const T*>(a.x) + (size_t)v * a.dim + off);
+                vaxpy_rn(val, c, xv);
+            }
         }
         if (a.epi & EPI_SCALE) {
             const T s = T(a.scale[v]);
@@ -146,6 +153,11 @@ __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32
         if (a.epi & EPI_RELU) {
 #pragma unroll
             for (int i = 0; i < VEC; ++i) val.a[i] = val.a[i] > T(0) ? val.a[i] : T(0);
+        }
+        if (a.epi & EPI_MASK) {
+            const Vec<T, VEC> m = ldv<T, VEC>(static_cast<const T*>(a.mask) + (size_t)v * a.dim + off);
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) val.a[i] = m.a[i] > T(0) ? val.a[i] : T(0);
         }
     }
     stv<T, VEC>(y, val);
@@ -212,7 +224,9 @@ struct K3Tune {
 // with width-TEAM shuffles, and UNR x KMAX 16-byte row vectors per lane are
 // in flight before the in-order adds.  Loop bounds are warp-uniform (max
 // over the warp's teams), loads/adds of finished teams are predicated off.
-template <class T, int VEC, int TEAM, int KMAX>
+// EW (fp32 path): per-edge weights ew[e] (CSR order) ride along with the
+// indices; acc += ew[e] * x[col[e]] (one FMA per element).
+template <class T, int VEC, int TEAM, int KMAX, bool EW = false>
 __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64_t e, uint32_t lane,
                                             const uint32_t (&off)[KMAX], const bool (&ok)[KMAX],
                                             Vec<T, VEC> (&acc)[KMAX]) {
@@ -224,10 +238,12 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
     const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
     for (uint32_t base = 0; base < wlen; base += 32) {
         uint32_t idxr[R];
+        float wr[EW ? R : 1];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t j = base + lane + r * TEAM;
             idxr[r] = j < len ? __ldg(col + b + j) : 0u;
+            if constexpr (EW) wr[r] = j < len ? __ldg(a.ew + b + j) : 0.f;
         }
         const uint32_t cnt = len > base ? min(32u, len - base) : 0u;
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, cnt);
@@ -235,8 +251,12 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
         for (int q0 = 0; q0 < 32; q0 += UNR) {
             if ((uint32_t)q0 >= wcnt) break;
             uint32_t idx[UNR];
+            float wgt[EW ? UNR : 1];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) idx[u] = __shfl_sync(0xffffffffu, idxr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
+            for (int u = 0; u < UNR; ++u) {
+                idx[u] = __shfl_sync(0xffffffffu, idxr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
+                if constexpr (EW) wgt[u] = __shfl_sync(0xffffffffu, wr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
+            }
             Vec<T, VEC> val[UNR][KMAX];
 #pragma unroll
             for (int u = 0; u < UNR; ++u)
@@ -248,13 +268,20 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
             for (int u = 0; u < UNR; ++u)
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k)
-                    if (ok[k] && (uint32_t)(q0 + u) < cnt) vadd(acc[k], val[u][k]);
+                    if (ok[k] && (uint32_t)(q0 + u) < cnt) {
+                        if constexpr (EW) {
+#pragma unroll
+                            for (int i = 0; i < VEC; ++i) acc[k].a[i] = fmaf(wgt[u], val[u][k].a[i], acc[k].a[i]);
+                        } else {
+                            vadd(acc[k], val[u][k]);
+                        }
+                    }
         }
     }
 }
 
 // ----------------------------------------------------------------- K3 ---
-template <class T, int VEC, int TEAM, int KMAX>
+template <class T, int VEC, int TEAM, int KMAX, bool EW>
 __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(AggArgs a) {
     using VT = Vec<T, VEC>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -280,7 +307,7 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(Ag
         VT acc[KMAX];
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) vzero(acc[k]);
-        gather_team<T, VEC, TEAM, KMAX>(a, b, e, lane, L.off, L.ok, acc);  // all lanes (b = e for idle teams)
+        gather_team<T, VEC, TEAM, KMAX, EW>(a, b, e, lane, L.off, L.ok, acc);  // all lanes (b = e for idle teams)
         if (active && direct) {
 #pragma unroll
             for (int k = 0; k < KMAX; ++k)
@@ -437,12 +464,20 @@ void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, con
     const size_t smem = (size_t)a.upc * kmax * TEAM * sizeof(Vec<T, VEC>);
     const unsigned threads = (a.upc * TEAM + 31) / 32 * 32;  // whole warps (gather_team is warp-collective)
     if (grid) {
-        if (kmax == 1)
-            k3_aggregate<T, VEC, TEAM, 1><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+        constexpr bool kEW = std::is_same<T, float>::value;  // weighted gathers: fp32 path only
+        if (a.ew && kEW) {
+            if (kmax == 1)
+                k3_aggregate<T, VEC, TEAM, 1, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            else if (kmax == 2)
+                k3_aggregate<T, VEC, TEAM, 2, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            else
+                k3_aggregate<T, VEC, TEAM, 4, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+        } else if (kmax == 1)
+            k3_aggregate<T, VEC, TEAM, 1, false><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
         else if (kmax == 2)
-            k3_aggregate<T, VEC, TEAM, 2><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            k3_aggregate<T, VEC, TEAM, 2, false><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
         else
-            k3_aggregate<T, VEC, TEAM, 4><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            k3_aggregate<T, VEC, TEAM, 4, false><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
         gnna::launched(ctx, "k3_aggregate");
     }
     const uint64_t nfix = plan->nsplit + plan->nempty;
@@ -493,15 +528,21 @@ void launch_k4(gnna_ctx* ctx, AggArgs& a, const Shape& s) {
 
 namespace gnna {
 
-// Scheduled aggregation over a plan (K3 + K3b).  epi/scale/alpha: epilogue.
-void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
-                    uint32_t epi, const float* scale, double alpha) {
+// Scheduled aggregation over a plan (K3 + K3b) with the optional epilogue
+// and per-edge weights of gnna_agg_opts (o may be null).
+void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                       const gnna_agg_opts* o) {
     if (!plan) raise(GNNA_ERR_DOMAIN, "null plan");
     if (dtype != GNNA_F32 && dtype != GNNA_F64) raise(GNNA_ERR_DOMAIN, "unknown dtype");
-    const uint32_t dim = plan->params.dim;
+    const uint32_t dim = (o && o->dim) ? o->dim : plan->params.dim;
     const int elem = dtype == GNNA_F32 ? 4 : 8;
+    if (o && o->edge_weight && dtype != GNNA_F32)
+        raise(GNNA_ERR_DOMAIN, "aggregate: edge weights are supported on the F32 path only");
     const uint32_t wpb = plan->wpb;
     const Shape s = choose_shape(elem, dim, plan->params.dw, pow2floor(256 / wpb), x, y);
+    // carry slots are sized for the widest dim seen on this plan
+    const uint64_t need = plan->ncarry * (uint64_t)dim * 8;
+    if (need > plan->carry.n) plan->carry = DevBuf<uint8_t>(need, ctx->stream);
     AggArgs a{};
     a.part_ptr = plan->part_ptr.get();
     a.part2node = plan->part2node.get();
@@ -518,9 +559,18 @@ void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mod
     a.nvec = dim / s.vec;
     a.kpl = s.kpl;
     a.seq = dim_mode == GNNA_DIM_SEQUENTIAL;
-    a.epi = epi;
-    a.scale = scale;
-    a.alpha = alpha;
+    if (o) {
+        if (o->self_weight || o->alpha != 0.0) a.epi |= EPI_SELF;
+        if (o->row_scale) a.epi |= EPI_SCALE;
+        if (o->relu) a.epi |= EPI_RELU;
+        if (o->mask) a.epi |= EPI_MASK;
+        a.sw = o->self_weight;
+        a.alpha = o->alpha;
+        a.scale = o->row_scale;
+        a.mask = o->mask;
+        // edge weights are indexed by absolute CSR position (same as col)
+        a.ew = o->edge_weight;
+    }
     if (plan->G == 0 && plan->nempty == 0) return;
     const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;
     if (grid > 0x7fffffffull) raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
@@ -531,6 +581,15 @@ void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mod
         if (s.vec == 2) launch_k3<double, 2>(ctx, a, s, grid, plan);
         else launch_k3<double, 1>(ctx, a, s, grid, plan);
     }
+}
+
+void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                    uint32_t epi, const float* scale, double alpha) {
+    gnna_agg_opts o{};
+    o.row_scale = (epi & EPI_SCALE) ? scale : nullptr;
+    o.alpha = (epi & EPI_SELF) ? alpha : 0.0;
+    o.relu = (epi & EPI_RELU) ? 1 : 0;
+    aggregate_plan_ex(ctx, plan, dtype, dim_mode, x, y, epi ? &o : nullptr);
 }
 
 // Row-order aggregation (K4).  mode 0 sum, 1 exact normalized, 2 exact GIN input.
@@ -579,6 +638,14 @@ void aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* row_ptr, const uin
 }  // namespace gnna
 
 extern "C" {
+
+gnna_status gnna_aggregate_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* d_x,
+                              void* d_y, const gnna_agg_opts* opts) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        gnna::aggregate_plan_ex(ctx, plan, dtype, dim_mode, d_x, d_y, opts);
+    });
+}
 
 gnna_status gnna_aggregate(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* d_x,
                            void* d_y) {

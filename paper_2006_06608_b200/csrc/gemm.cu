@@ -300,3 +300,12 @@ extern "C" gnna_status gnna_gemm(gnna_ctx* ctx, int dtype, const void* d_a, uint
         gnna::gemm(ctx, dtype, d_a, m, k, d_w, n_out, d_bias, epilogue, d_row_scale, d_out);
     });
 }
+
+extern "C" gnna_status gnna_gemm_tn(gnna_ctx* ctx, int dtype, const void* d_a, const void* d_b, uint32_t m, uint32_t p,
+                                    uint32_t q, void* d_out) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        gnna::gemm_tn(ctx, dtype, d_a, d_b, m, p, q, d_out);
+    });
+}

@@ -138,7 +138,7 @@ struct gnna_plan {
     gnna::DevBuf<uint32_t> fix_nodes;  // nsplit + nempty: split nodes then empty rows
     gnna::DevBuf<uint32_t> fix_first;  // nsplit: first carry index
     gnna::DevBuf<uint32_t> fix_count;  // nsplit: carries per split node
-    gnna::DevBuf<uint8_t> carry;       // ncarry * dim * 8 bytes
+    mutable gnna::DevBuf<uint8_t> carry;  // ncarry * dim * 8 bytes (grown for wider dims)
 };
 
 // Unit flag bits (plan.cu builds them, aggregate.cu consumes them).

@@ -19,6 +19,7 @@
 // Â^T is evaluated on the transposed CSR (d_rt_*) with the forward norms;
 // for the symmetric graphs to_csr(.., true) builds it is the CSR itself.
 #include <algorithm>
+#include <memory>
 #include <vector>
 
 #include "gnna_common.cuh"
@@ -60,6 +61,23 @@ __global__ void k5_gcn_norm(const uint64_t* __restrict__ row_ptr, const uint32_t
         if (deg == 0) deg = 1;
         norm[v] = 1.0 / sqrt((double)deg);
         if (self) self[v] = imp;
+    }
+}
+
+// fp32 operands of the fused normalized aggregation: row scale / self
+// weight per node, and per-edge weights norm[col[e]] (warp per row).
+__global__ void k5_gcn_weights(const uint64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t n,
+                               const double* __restrict__ norm, const uint8_t* __restrict__ self,
+                               float* __restrict__ rs, float* __restrict__ sw, float* __restrict__ ew) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t v = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; v < n; v += warps) {
+        if (lane == 0) {
+            if (rs) rs[v] = (float)norm[v];
+            if (sw) sw[v] = self[v] ? (float)norm[v] : 0.f;
+        }
+        if (ew)
+            for (uint64_t p = row_ptr[v] + lane; p < row_ptr[v + 1]; p += 32) ew[p] = (float)norm[col[p]];
     }
 }
 
@@ -129,6 +147,95 @@ double dot(gnna_ctx* ctx, int dtype, const void* a, const void* b, uint64_t coun
     return s;
 }
 
+// ---------------------------------------------------------- F32 fast path
+// The fp32 layer entry points run on a scheduled plan (K1/K2 units, K3 with
+// fused epilogues) instead of K4's row-per-team loop, so power-law hubs are
+// split into workload units.  Parameters come from the evaluator
+// (auto_params on the graph's degree statistics, B200 profile).
+void check(gnna_ctx* ctx, gnna_status st) {
+    if (st != GNNA_OK) gnna::raise(st, ctx->err);
+}
+
+struct TransientPlan {
+    gnna_plan* p = nullptr;
+    TransientPlan(gnna_ctx* ctx, const uint64_t* rp, const uint32_t* col, uint32_t n, uint32_t dim) {
+        gnna_model_inputs mi{};
+        check(ctx, gnna_model_inputs_from_graph(ctx, rp, n, dim, &mi));
+        check(ctx, gnna_b200_profile(ctx, &mi));
+        gnna_params prm{};
+        if (gnna_auto_params(&mi, &prm) != GNNA_OK) prm = gnna_params{16, 32, 128, 32, dim};
+        prm.dim = dim;
+        check(ctx, gnna_plan_create(ctx, rp, col, n, 0, n, &prm, GNNA_WARP_SHARED, &p));
+    }
+    ~TransientPlan() {
+        if (p) gnna_plan_destroy(p);
+    }
+};
+
+// Row scale / self weight / per-edge weights of D^-1/2 (A [+I]) D^-1/2 with
+// the norms of the forward CSR (fwd) laid out on the CSR being aggregated
+// (tgt: the forward CSR itself, or its transpose for the adjoint).
+struct GcnWeights {
+    DevBuf<float> rs, sw, ew;
+    GcnWeights(gnna_ctx* ctx, const uint64_t* fwd_rp, const uint32_t* fwd_col, const uint64_t* tgt_rp,
+               const uint32_t* tgt_col, uint32_t n, int add_self) {
+        uint64_t nnz = 0;
+        gnna::to_host(ctx, &nnz, tgt_rp + n, 1);
+        rs = DevBuf<float>(n ? n : 1, ctx->stream);
+        sw = DevBuf<float>(n ? n : 1, ctx->stream);
+        ew = DevBuf<float>(nnz ? nnz : 1, ctx->stream);
+        if (!n) return;
+        DevBuf<double> norm(n, ctx->stream);
+        DevBuf<uint8_t> self(n, ctx->stream);
+        gcn_norm(ctx, fwd_rp, fwd_col, n, add_self, norm.get(), self.get());
+        k5_gcn_weights<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, ctx->stream>>>(
+            tgt_rp, tgt_col, n, norm.get(), self.get(), rs.get(), sw.get(), ew.get());
+        gnna::launched(ctx, "k5_gcn_weights");
+    }
+    gnna_agg_opts opts(uint32_t dim) const {
+        gnna_agg_opts o{};
+        o.dim = dim;
+        o.edge_weight = ew.get();
+        o.self_weight = sw.get();
+        o.row_scale = rs.get();
+        return o;
+    }
+};
+
+}  // namespace
+
+namespace gnna {
+void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                       const gnna_agg_opts* o);
+}
+
+namespace {
+
+void fast_gcn_forward(gnna_ctx* ctx, const uint64_t* rp, const uint32_t* col, uint32_t n, const void* x,
+                      uint32_t in_dim, const void* w, uint32_t out_dim, int add_self, void* y) {
+    if (!n) return;
+    TransientPlan plan(ctx, rp, col, n, std::min(in_dim, out_dim));
+    GcnWeights gw(ctx, rp, col, rp, col, n, add_self);
+    if (out_dim < in_dim) {
+        DevBuf<float> t((size_t)n * out_dim, ctx->stream);
+        gnna::gemm(ctx, GNNA_F32, x, n, in_dim, w, out_dim, nullptr, 0, nullptr, t.get());
+        const gnna_agg_opts o = gw.opts(out_dim);
+        gnna::aggregate_plan_ex(ctx, plan.p, GNNA_F32, GNNA_DIM_CYCLIC, t.get(), y, &o);
+    } else {
+        DevBuf<float> z((size_t)n * in_dim, ctx->stream);
+        const gnna_agg_opts o = gw.opts(in_dim);
+        gnna::aggregate_plan_ex(ctx, plan.p, GNNA_F32, GNNA_DIM_CYCLIC, x, z.get(), &o);
+        gnna::gemm(ctx, GNNA_F32, z.get(), n, in_dim, w, out_dim, nullptr, 0, nullptr, y);
+    }
+}
+
+void fast_gin_aggregate(gnna_ctx* ctx, const gnna_plan* plan, const void* x, uint32_t dim, double eps, void* z) {
+    gnna_agg_opts o{};
+    o.dim = dim;
+    o.alpha = 1.0 + eps;
+    gnna::aggregate_plan_ex(ctx, plan, GNNA_F32, GNNA_DIM_CYCLIC, x, z, &o);
+}
+
 }  // namespace
 
 extern "C" {
@@ -138,6 +245,20 @@ gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
         gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, d_norm, d_self);
+    });
+}
+
+gnna_status gnna_gcn_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                             int add_self_loops, float* d_row_scale, float* d_self_weight, float* d_edge_weight) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (!n) return;
+        DevBuf<double> norm(n, ctx->stream);
+        DevBuf<uint8_t> self(n, ctx->stream);
+        gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, norm.get(), self.get());
+        k5_gcn_weights<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, ctx->stream>>>(
+            d_row_ptr, d_col, n, norm.get(), self.get(), d_row_scale, d_self_weight, d_edge_weight);
+        gnna::launched(ctx, "k5_gcn_weights");
     });
 }
 
@@ -159,6 +280,10 @@ gnna_status gnna_gcn_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr
         gnna::require_ctx(ctx);
         const size_t es = esize(dtype);
         check_dims(in_dim, out_dim);
+        if (dtype == GNNA_F32) {
+            fast_gcn_forward(ctx, d_row_ptr, d_col, n, d_x, in_dim, d_w, out_dim, add_self_loops, d_y);
+            return;
+        }
         cudaStream_t s = ctx->stream;
         DevBuf<double> norm(n ? n : 1, s);
         DevBuf<uint8_t> self(n ? n : 1, s);
@@ -184,13 +309,53 @@ gnna_status gnna_gin_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr
         check_dims(in_dim, out_dim);
         if (!d_b) gnna::raise(GNNA_ERR_DOMAIN, "gin: null bias");
         DevBuf<uint8_t> z((size_t)n * in_dim * es + 1, ctx->stream);
-        // engine.cpp:394-400: z = sum_N x (CSR order), then z += (1+eps) x
-        gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, in_dim, d_x, z.get(), 2, nullptr, nullptr, 1.0 + eps,
-                             0, nullptr);
+        if (dtype == GNNA_F32) {
+            if (n) {
+                TransientPlan plan(ctx, d_row_ptr, d_col, n, in_dim);
+                fast_gin_aggregate(ctx, plan.p, d_x, in_dim, eps, z.get());
+            }
+        } else {
+            // engine.cpp:394-400: z = sum_N x (CSR order), then z += (1+eps) x
+            gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, in_dim, d_x, z.get(), 2, nullptr, nullptr,
+                                 1.0 + eps, 0, nullptr);
+        }
         // engine.cpp:401-406: h = z·W, relu(h + b)
         gnna::gemm(ctx, dtype, z.get(), n, in_dim, d_w, out_dim, d_b, 1, nullptr, d_y);
     });
 }
+
+namespace {
+// Normalized aggregation for one direction of the backward pass: exact K4
+// (F64) or the scheduled fast path (F32, norms of the forward CSR).
+struct NormAgg {
+    gnna_ctx* ctx;
+    int dtype;
+    const uint64_t* rp;
+    const uint32_t* col;
+    uint32_t n;
+    const double* norm;
+    const uint8_t* self;
+    std::unique_ptr<TransientPlan> plan;
+    std::unique_ptr<GcnWeights> w;
+    NormAgg(gnna_ctx* c, int dt, const uint64_t* fwd_rp, const uint32_t* fwd_col, const uint64_t* r,
+            const uint32_t* cl, uint32_t nn, const double* nrm, const uint8_t* slf, int add_self, uint32_t dim)
+        : ctx(c), dtype(dt), rp(r), col(cl), n(nn), norm(nrm), self(slf) {
+        if (dt == GNNA_F32 && nn) {
+            plan = std::make_unique<TransientPlan>(c, r, cl, nn, dim);
+            w = std::make_unique<GcnWeights>(c, fwd_rp, fwd_col, r, cl, nn, add_self);
+        }
+    }
+    void operator()(const void* x, void* y, uint32_t dim) const {
+        if (dtype == GNNA_F32) {
+            if (!n) return;
+            const gnna_agg_opts o = w->opts(dim);
+            gnna::aggregate_plan_ex(ctx, plan->p, GNNA_F32, GNNA_DIM_CYCLIC, x, y, &o);
+        } else {
+            normalized(ctx, dtype, rp, col, n, dim, norm, self, x, y);
+        }
+    }
+};
+}  // namespace
 
 gnna_status gnna_gcn_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr, const uint32_t* d_col,
                               const uint64_t* d_rt_ptr, const uint32_t* d_rt_col, uint32_t n, const void* d_x,
@@ -207,17 +372,22 @@ gnna_status gnna_gcn_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_pt
         gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, norm.get(), self.get());
         DevBuf<uint8_t> wt((size_t)in_dim * out_dim * es, s);
         gnna::transpose(ctx, dtype, d_w, in_dim, out_dim, wt.get());  // out x in
+        const uint32_t adim = std::min(in_dim, out_dim);
+        const NormAgg adj(ctx, dtype, d_row_ptr, d_col, d_rt_ptr, d_rt_col, n, norm.get(), self.get(), add_self_loops,
+                          adim);
         if (out_dim < in_dim) {
             DevBuf<uint8_t> dh((size_t)n * out_dim * es + 1, s);
-            normalized(ctx, dtype, d_rt_ptr, d_rt_col, n, out_dim, norm.get(), self.get(), d_dy, dh.get());
+            adj(d_dy, dh.get(), out_dim);  // dH = Â^T dY
             gnna::gemm_tn(ctx, dtype, d_x, dh.get(), n, in_dim, out_dim, d_dw);
             gnna::gemm(ctx, dtype, dh.get(), n, out_dim, wt.get(), in_dim, nullptr, 0, nullptr, d_dx);
         } else {
+            const NormAgg fwd(ctx, dtype, d_row_ptr, d_col, d_row_ptr, d_col, n, norm.get(), self.get(),
+                              add_self_loops, in_dim);
             DevBuf<uint8_t> z((size_t)n * in_dim * es + 1, s), dz((size_t)n * in_dim * es + 1, s);
-            normalized(ctx, dtype, d_row_ptr, d_col, n, in_dim, norm.get(), self.get(), d_x, z.get());
+            fwd(d_x, z.get(), in_dim);  // Z = Â X
             gnna::gemm_tn(ctx, dtype, z.get(), d_dy, n, in_dim, out_dim, d_dw);
             gnna::gemm(ctx, dtype, d_dy, n, out_dim, wt.get(), in_dim, nullptr, 0, nullptr, dz.get());
-            normalized(ctx, dtype, d_rt_ptr, d_rt_col, n, in_dim, norm.get(), self.get(), dz.get(), d_dx);
+            adj(dz.get(), d_dx, in_dim);  // dX = Â^T dZ
         }
     });
 }
@@ -234,8 +404,14 @@ gnna_status gnna_gin_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_pt
         cudaStream_t s = ctx->stream;
         const size_t nz = (size_t)n * in_dim * es + 1, nu = (size_t)n * out_dim * es + 1;
         DevBuf<uint8_t> z(nz, s), u(nu, s), du(nu, s), dz(nz, s), wt((size_t)in_dim * out_dim * es, s);
-        gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, in_dim, d_x, z.get(), 2, nullptr, nullptr, 1.0 + eps,
-                             0, nullptr);
+        std::unique_ptr<TransientPlan> pf, pt;
+        if (dtype == GNNA_F32 && n) {
+            pf = std::make_unique<TransientPlan>(ctx, d_row_ptr, d_col, n, in_dim);
+            fast_gin_aggregate(ctx, pf->p, d_x, in_dim, eps, z.get());
+        } else {
+            gnna::aggregate_rows(ctx, dtype, d_row_ptr, d_col, 0, n, in_dim, d_x, z.get(), 2, nullptr, nullptr,
+                                 1.0 + eps, 0, nullptr);
+        }
         gnna::gemm(ctx, dtype, z.get(), n, in_dim, d_w, out_dim, nullptr, 0, nullptr, u.get());
         const uint64_t mq = (uint64_t)n * out_dim;
         if (mq) {
@@ -253,9 +429,15 @@ gnna_status gnna_gin_backward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_pt
         gnna::gemm_tn(ctx, dtype, z.get(), du.get(), n, in_dim, out_dim, d_dw);
         gnna::transpose(ctx, dtype, d_w, in_dim, out_dim, wt.get());
         gnna::gemm(ctx, dtype, du.get(), n, out_dim, wt.get(), in_dim, nullptr, 0, nullptr, dz.get());
-        // dX = A^T dZ + (1+eps) dZ: K4 mode 2 over the transposed CSR
-        gnna::aggregate_rows(ctx, dtype, d_rt_ptr, d_rt_col, 0, n, in_dim, dz.get(), d_dx, 2, nullptr, nullptr,
-                             1.0 + eps, 0, nullptr);
+        // dX = A^T dZ + (1+eps) dZ over the transposed CSR
+        if (dtype == GNNA_F32 && n) {
+            const bool same = d_rt_ptr == d_row_ptr && d_rt_col == d_col;
+            if (!same) pt = std::make_unique<TransientPlan>(ctx, d_rt_ptr, d_rt_col, n, in_dim);
+            fast_gin_aggregate(ctx, same ? pf->p : pt->p, dz.get(), in_dim, eps, d_dx);
+        } else {
+            gnna::aggregate_rows(ctx, dtype, d_rt_ptr, d_rt_col, 0, n, in_dim, dz.get(), d_dx, 2, nullptr, nullptr,
+                                 1.0 + eps, 0, nullptr);
+        }
         if (deps) *deps = dot(ctx, dtype, d_x, dz.get(), (uint64_t)n * in_dim);
     });
 }

@@ -1,0 +1,122 @@
+"""GNN models on the B200 path: the BASELINE C3 configuration (2-layer GCN,
+forward + backward + SGD step) and a GIN layer, composed from the C-ABI's
+plan-based kernels (fp32 perf path):
+
+  aggregation  gnna_aggregate_ex on one gnna_plan (K1/K2 built once), with the
+               normalisation fused in: per-edge weights norm[col[e]], self
+               weight, row scale norm[v], and the ReLU / ReLU-backward mask in
+               the flush epilogue
+  update       gnna_gemm (K6) and its transposed forms for the gradients
+
+Layer math follows gcn_layer (engine.cpp:373-382): update first iff the layer
+shrinks the width, z = D^-1/2 (A [+I]) D^-1/2 x.  The reference has no model
+or backward; a ReLU between the two layers makes it the standard
+2-layer GCN.  torch supplies device memory and the tiny SGD update (plumbing).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .capi import WARP_SHARED, Context, Params
+
+
+class GCN2:
+    """2-layer GCN: y = Â relu(Â x W1) W2 (each layer ordered as gcn_layer)."""
+
+    def __init__(self, ctx: Context, row_ptr, col, in_dim, hidden, out_dim, self_loops=False, params: Params = None,
+                 seed=4, lr=0.01):
+        self.ctx, self.torch = ctx, torch
+        self.row_ptr, self.col = row_ptr, col
+        self.n = row_ptr.numel() - 1
+        self.dims = (in_dim, hidden, out_dim)
+        dev = row_ptr.device
+        if params is None:
+            params = ctx.auto_params(ctx.model_inputs(row_ptr, min(hidden, in_dim), b200=True))
+        self.params = params
+        # one schedule (K1 units + K2 Algorithm-1 plan) for every aggregation of the step
+        self.plan = ctx.plan(row_ptr, col, params, WARP_SHARED)
+        self.rs, self.sw, self.ew = ctx.gcn_weights(row_ptr, col, self_loops)
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        self.w1 = ((torch.rand((in_dim, hidden), generator=g, device=dev) * 2 - 1) / math.sqrt(in_dim)).contiguous()
+        g.manual_seed(seed + 1)
+        self.w2 = ((torch.rand((hidden, out_dim), generator=g, device=dev) * 2 - 1) / math.sqrt(hidden)).contiguous()
+        self.zero_b1 = torch.zeros(hidden, device=dev)
+        self.lr = lr
+
+    def _agg(self, x, relu=False, mask=None, out=None):
+        return self.plan.aggregate_ex(x, out=out, edge_weight=self.ew, self_weight=self.sw, row_scale=self.rs,
+                                      relu=relu, mask=mask)
+
+    def forward(self, x):
+        ctx = self.ctx
+        in_dim, hid, out_dim = self.dims
+        s = {}
+        if hid < in_dim:  # layer 1 update first: h1 = relu(Â (x W1))
+            s["t1"] = ctx.gemm(x, self.w1)
+            s["h1"] = self._agg(s["t1"], relu=True)
+        else:  # aggregate first: h1 = relu((Â x) W1)
+            s["z1"] = self._agg(x)
+            s["h1"] = ctx.gemm(s["z1"], self.w1, self.zero_b1, 1)
+        if out_dim < hid:  # layer 2 update first
+            s["t2"] = ctx.gemm(s["h1"], self.w2)
+            y = self._agg(s["t2"])
+        else:
+            s["z2"] = self._agg(s["h1"])
+            y = ctx.gemm(s["z2"], self.w2)
+        self.saved = s
+        return y
+
+    def backward(self, x, dy):
+        """Gradients of <dy, forward(x)> w.r.t. W1, W2 (Â is symmetric for the
+        symmetrised CSR to_csr(.., true) builds, so Â^T = Â)."""
+        ctx, s = self.ctx, self.saved
+        in_dim, hid, out_dim = self.dims
+        w1t, w2t = self.w1.t().contiguous(), self.w2.t().contiguous()
+        if out_dim < hid:
+            dt2 = self._agg(dy)                                    # Â^T dY
+            dw2 = ctx_gemm_tn(ctx, s["h1"], dt2)                   # h1^T dT2
+            dh1 = ctx.gemm(dt2, w2t)
+            dp1 = dh1 * (s["h1"] > 0)
+        else:
+            dw2 = ctx_gemm_tn(ctx, s["z2"], dy)                    # (Â h1)^T dY
+            dz2 = ctx.gemm(dy, w2t)                                # dY W2^T
+            dp1 = self._agg(dz2, mask=s["h1"])                     # Â^T dZ2, masked by relu'(h1)
+        if hid < in_dim:
+            dt1 = self._agg(dp1)                                   # Â^T dP1
+            dw1 = ctx_gemm_tn(ctx, x, dt1)                         # x^T dT1
+        else:
+            dw1 = ctx_gemm_tn(ctx, s["z1"], dp1)
+        return dw1, dw2
+
+    def sgd(self, dw1, dw2):
+        self.w1.sub_(self.lr * dw1)
+        self.w2.sub_(self.lr * dw2)
+
+    def step(self, x, dy):
+        y = self.forward(x)
+        dw1, dw2 = self.backward(x, dy)
+        self.sgd(dw1, dw2)
+        return y, dw1, dw2
+
+    def aggregations_per_step(self):
+        """(count, width) of the aggregations one step runs."""
+        in_dim, hid, out_dim = self.dims
+        widths = [min(hid, in_dim), min(out_dim, hid), min(out_dim, hid)]
+        if hid < in_dim:
+            widths.append(hid)
+        return widths
+
+
+def ctx_gemm_tn(ctx: Context, a, b):
+    """a^T b through the C-ABI (deterministic chunked reduction)."""
+    import ctypes as C
+    from .capi import _dtype_code, _ptr
+    m, p = a.shape
+    q = b.shape[1]
+    out = torch.empty((p, q), dtype=a.dtype, device=a.device)
+    ctx._check(ctx.L.gnna_gemm_tn(ctx.h, C.c_int(_dtype_code(a)), _ptr(a), _ptr(b), C.c_uint32(m), C.c_uint32(p),
+                                  C.c_uint32(q), _ptr(out)))
+    return out

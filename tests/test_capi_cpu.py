@@ -219,4 +219,4 @@ def test_row_sharded_allgather_gloo_world2(tmp_path):
         if r.returncode == 0 or "AssertionError" in r.stderr:
             break
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    assert r.stdout.count(" ok ") == 2
+    assert r.stdout.count("ok") == 2  # one per rank (the two ranks' lines may interleave)

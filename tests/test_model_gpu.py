@@ -1,0 +1,122 @@
+"""GPU: the fused aggregation options (gnna_aggregate_ex) and the 2-layer GCN
+training step (paper_2006_06608_b200/gcn.py) built on them.
+
+* aggregate_ex: per-edge weights, self weights, row scale, ReLU and the
+  ReLU-backward mask, at widths other than the plan's, on power-law graphs
+  whose hubs span many schedule blocks (carry path), vs an fp64 numpy
+  restatement; fp32 bar 1e-5 relative to sum|terms|.
+* GCN2: forward vs two REFERENCE-semantics gcn_layer calls (oracle, fp64) with
+  a ReLU between; full step gradients vs torch float64 autograd.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_graph, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def powerlaw_graph(orc, rng, n, e, a=0.8):
+    w = 1.0 / np.arange(1, n + 1) ** a
+    src = rng.choice(n, size=e, p=w / w.sum())
+    edges = np.stack([src, rng.integers(0, n, size=e)], 1).astype(np.uint32)
+    return orc.to_csr(n, edges, True)
+
+
+def ref_agg(rp, col, x, ew=None, sw=None, alpha=0.0, rs=None, relu=False, mask=None):
+    n = len(rp) - 1
+    y = np.zeros_like(x, dtype=np.float64)
+    bound = np.zeros_like(y)
+    for v in range(n):
+        nb = col[rp[v]:rp[v + 1]]
+        w = ew[rp[v]:rp[v + 1]] if ew is not None else np.ones(len(nb))
+        y[v] = (w[:, None] * x[nb]).sum(0)
+        bound[v] = (np.abs(w)[:, None] * np.abs(x[nb])).sum(0)
+        c = sw[v] if sw is not None else alpha
+        y[v] += c * x[v]
+        bound[v] += abs(c) * np.abs(x[v])
+        if rs is not None:
+            y[v] *= rs[v]
+            bound[v] *= abs(rs[v])
+    if relu:
+        y = np.maximum(y, 0)
+    if mask is not None:
+        y = np.where(mask > 0, y, 0)
+    return y, bound
+
+
+def test_aggregate_ex_options(ctx, orc):
+    from paper_2006_06608_b200.capi import Params
+    rng = np.random.default_rng(40)
+    for t in range(8):
+        n = int(rng.integers(50, 6000))
+        rp, col = powerlaw_graph(orc, rng, n, 6 * n)
+        drp, dcol = to_dev(rp, col)
+        plan_dim = int(rng.choice([16, 64]))
+        p = Params.make(ngs=int(rng.choice([4, 16, 64])), dw=32, tpb=int(rng.choice([64, 128, 256])), dim=plan_dim)
+        plan = ctx.plan(drp, dcol, p, 2)
+        for dim in (16, 22, 64, 3):
+            x = rng.random((n, dim)) - 0.3
+            ew = rng.random(len(col)).astype(np.float32)
+            sw = (rng.random(n) * (rng.random(n) < 0.5)).astype(np.float32)
+            rs = rng.random(n).astype(np.float32)
+            mask = rng.random((n, dim)) - 0.5
+            dx = to_dev(x.astype(np.float32))
+            opts = [dict(), dict(ew=ew), dict(ew=ew, sw=sw, rs=rs), dict(alpha=1.5), dict(ew=ew, rs=rs, relu=True),
+                    dict(sw=sw, mask=mask)]
+            for o in opts:
+                want, bound = ref_agg(rp, col, x.astype(np.float32).astype(np.float64), o.get("ew"), o.get("sw"),
+                                      o.get("alpha", 0.0), o.get("rs"), o.get("relu", False), o.get("mask"))
+                got = plan.aggregate_ex(dx, edge_weight=to_dev(o["ew"]) if "ew" in o else None,
+                                        self_weight=to_dev(o["sw"]) if "sw" in o else None,
+                                        alpha=o.get("alpha", 0.0), row_scale=to_dev(o["rs"]) if "rs" in o else None,
+                                        relu=o.get("relu", False),
+                                        mask=to_dev(o["mask"].astype(np.float32)) if "mask" in o else None)
+                got = got.cpu().numpy().astype(np.float64)
+                err = np.abs(got - want)
+                assert (err <= 1e-5 * (bound + np.abs(want)) + 1e-30).all(), (t, dim, list(o), float(err.max()))
+
+
+def dense_norm_adj(rp, col, self_loops):
+    n = len(rp) - 1
+    A = np.zeros((n, n))
+    for v in range(n):
+        A[v, col[rp[v]:rp[v + 1]]] = 1.0
+    if self_loops:
+        for v in range(n):
+            if A[v, v] == 0:
+                A[v, v] = 1.0
+    deg = np.maximum(A.sum(1), 1)
+    d = 1 / np.sqrt(deg)
+    return d[:, None] * A * d[None, :]
+
+
+@pytest.mark.parametrize("dims,sl", [((96, 16, 22), False), ((12, 32, 8), True), ((20, 16, 16), False)])
+def test_gcn2_step_vs_autograd_and_reference(ctx, orc, dims, sl):
+    from paper_2006_06608_b200.gcn import GCN2
+    rng = np.random.default_rng(sum(dims))
+    n = 700
+    rp, col = powerlaw_graph(orc, rng, n, 3000)
+    drp, dcol = to_dev(rp, col)
+    din, hid, dout = dims
+    model = GCN2(ctx, drp, dcol, din, hid, dout, self_loops=sl, lr=0.0)
+    x = (rng.random((n, din)) - 0.5).astype(np.float32)
+    dy = (rng.random((n, dout)) - 0.5).astype(np.float32)
+    w1, w2 = model.w1.double().cpu().numpy(), model.w2.double().cpu().numpy()
+    y, dw1, dw2 = model.step(to_dev(x), to_dev(dy))
+    # reference semantics: gcn_layer (oracle, fp64) twice with a ReLU between
+    h1 = np.maximum(orc.gcn_layer(rp, col, x.astype(np.float64), w1, sl), 0)
+    want = orc.gcn_layer(rp, col, h1, w2, sl)
+    scale = np.abs(want).max()
+    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=1e-4, atol=1e-5 * scale)
+    # gradients: torch float64 autograd
+    An = torch.tensor(dense_norm_adj(rp, col, sl))
+    W1 = torch.tensor(w1, requires_grad=True)
+    W2 = torch.tensor(w2, requires_grad=True)
+    X = torch.tensor(x, dtype=torch.float64)
+    Y = An @ torch.relu(An @ X @ W1) @ W2
+    Y.backward(torch.tensor(dy, dtype=torch.float64))
+    for got, ref in ((dw1, W1.grad), (dw2, W2.grad)):
+        r = ref.numpy()
+        np.testing.assert_allclose(got.double().cpu().numpy(), r, rtol=1e-3, atol=1e-4 * np.abs(r).max())
