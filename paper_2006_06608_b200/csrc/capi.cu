@@ -29,6 +29,15 @@ gnna_status gnna_create(int device, gnna_ctx** out) {
             gnna::raise(GNNA_ERR_CUDA, "libgnna is built for sm_100a (B200); device is sm_" +
                                            std::to_string(major) + std::to_string(minor));
         GNNA_CUDA(cudaSetDevice(device));
+        // Scratch buffers come from the stream-ordered pool.  Its default
+        // release threshold (0) hands memory back to the OS at every stream
+        // sync, so the next cudaMallocAsync re-maps it (~100 us per call on
+        // large buffers); keep freed memory cached in the pool instead.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         auto ctx = new gnna_ctx();
         ctx->device = device;
         cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);

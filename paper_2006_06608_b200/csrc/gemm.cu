@@ -16,6 +16,7 @@
 // gemm_tn (dW = A^T B, a reduction over all rows) is split over row chunks
 // with per-chunk partials summed in chunk order: deterministic.
 #include <algorithm>
+#include <type_traits>
 
 #include "gnna_common.cuh"
 
@@ -187,9 +188,358 @@ __global__ void k6_colsum_partial(const T* __restrict__ b, uint32_t m, uint32_t 
     }
 }
 
+// ------------------------------------------------------ fp32 fast kernels
+// X·W for skinny W (n <= 32): one output row per thread, A staged through
+// shared memory in coalesced 32-column chunks (row stride 33: conflict-free
+// column reads), W chunk in shared memory read as float4 broadcasts, NJ
+// accumulators in registers (NJ = n rounded up to 4, 8, 16 or 32).  Per k:
+// 1 + NJ/4 shared loads for NJ FMAs; the kernel streams A at HBM speed.
+template <int NJ>
+__global__ void __launch_bounds__(ROWS) k6_gemm_f32(GemmArgs g) {
+    __shared__ float sa[ROWS][KC + 1];
+    __shared__ __align__(16) float sw[KC][NJ];
+    const float* __restrict__ a = static_cast<const float*>(g.a);
+    const float* __restrict__ w = static_cast<const float*>(g.w);
+    const uint64_t row0 = (uint64_t)blockIdx.x * ROWS;
+    const uint32_t j0 = blockIdx.y * NJ;
+    const uint32_t nj = g.n - j0 < (uint32_t)NJ ? g.n - j0 : (uint32_t)NJ;
+    const uint32_t t = threadIdx.x;
+    float acc[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+    const bool vec4 = (g.k % 4 == 0) && ((uintptr_t)a % 16 == 0);
+    for (uint32_t k0 = 0; k0 < g.k; k0 += KC) {
+        const uint32_t kc = g.k - k0 < (uint32_t)KC ? g.k - k0 : (uint32_t)KC;
+        if (vec4) {
+            // 8 independent 16-byte loads per thread in flight (ROWS x KC / 4 / ROWS)
+            float4 v[ROWS * KC / 4 / ROWS];
+#pragma unroll
+            for (int i = 0; i < ROWS * KC / 4 / ROWS; ++i) {
+                const uint32_t e = t + i * ROWS;
+                const uint32_t r = e / (KC / 4), c4 = e % (KC / 4);
+                const uint64_t gr = row0 + r;
+                v[i] = (gr < g.m && c4 * 4 < kc)
+                           ? __ldg(reinterpret_cast<const float4*>(a + gr * g.k + k0) + c4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < ROWS * KC / 4 / ROWS; ++i) {
+                const uint32_t e = t + i * ROWS;
+                const uint32_t r = e / (KC / 4), c = (e % (KC / 4)) * 4;
+                sa[r][c] = v[i].x;
+                sa[r][c + 1] = v[i].y;
+                sa[r][c + 2] = v[i].z;
+                sa[r][c + 3] = v[i].w;
+            }
+        } else {
+#pragma unroll 4
+            for (uint32_t e = t; e < ROWS * KC; e += ROWS) {
+                const uint32_t r = e / KC, c = e % KC;
+                const uint64_t gr = row0 + r;
+                sa[r][c] = (gr < g.m && c < kc) ? __ldg(a + gr * g.k + k0 + c) : 0.f;
+            }
+        }
+        for (uint32_t e = t; e < KC * NJ; e += ROWS) {
+            const uint32_t r = e / NJ, c = e % NJ;
+            sw[r][c] = (r < kc && c < nj) ? __ldg(w + (uint64_t)(k0 + r) * g.n + j0 + c) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (uint32_t kk = 0; kk < (uint32_t)KC; ++kk) {
+            const float av = sa[t][kk];
+#pragma unroll
+            for (int j = 0; j < NJ; j += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(&sw[kk][j]);
+                acc[j] = fmaf(av, w4.x, acc[j]);
+                acc[j + 1] = fmaf(av, w4.y, acc[j + 1]);
+                acc[j + 2] = fmaf(av, w4.z, acc[j + 2]);
+                acc[j + 3] = fmaf(av, w4.w, acc[j + 3]);
+            }
+        }
+        __syncthreads();
+    }
+    const uint64_t r = row0 + t;
+    if (r >= g.m) return;
+    float* o = static_cast<float*>(g.out) + r * g.n + j0;
+    const float* b = g.epilogue == 1 ? static_cast<const float*>(g.bias) + j0 : nullptr;
+    const float s = g.epilogue == 2 ? (float)g.row_scale[r] : 1.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (j >= (int)nj) break;
+        float v = acc[j];
+        if (g.epilogue == 1) {
+            v += b[j];
+            v = v > 0.f ? v : 0.f;
+        } else if (g.epilogue == 2) {
+            v *= s;
+        }
+        o[j] = v;
+    }
+}
+
+// X·W, row per thread with DIRECT 16-byte loads of the thread's own A row
+// (no A staging, no barriers in the k loop): a warp instruction reads 16 B of
+// 32 rows, the next instruction the following 16 B (L1 hits), so DRAM sees
+// each A byte once while every thread keeps KCH/4 loads in flight, and the
+// next k chunk is prefetched while the current one is consumed.  W lives in
+// shared memory for the whole kernel (read as float4 broadcasts).
+// Requires k % 4 == 0, 16-byte aligned A, k*NJ*4 <= 64 KiB.
+template <int NJ>
+__global__ void __launch_bounds__(128) k6_gemm_rows(GemmArgs g) {
+    constexpr int KCH = 16;  // k values per prefetch chunk (4 float4)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* sw = reinterpret_cast<float*>(smem_raw);  // [k][NJ]
+    const float* __restrict__ w = static_cast<const float*>(g.w);
+    const uint32_t j0 = blockIdx.y * NJ;
+    const uint32_t nj = g.n - j0 < (uint32_t)NJ ? g.n - j0 : (uint32_t)NJ;
+    for (uint32_t e = threadIdx.x; e < g.k * NJ; e += blockDim.x) {
+        const uint32_t r = e / NJ, c = e % NJ;
+        sw[e] = c < nj ? __ldg(w + (uint64_t)r * g.n + j0 + c) : 0.f;
+    }
+    __syncthreads();
+    const uint64_t row = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= g.m) return;
+    const float4* __restrict__ arow = reinterpret_cast<const float4*>(static_cast<const float*>(g.a) + row * g.k);
+    float acc[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+    const uint32_t nch = g.k / KCH, tail = g.k % KCH;
+    float4 cur[KCH / 4], nxt[KCH / 4];
+    if (nch) {
+#pragma unroll
+        for (int i = 0; i < KCH / 4; ++i) cur[i] = __ldg(arow + i);
+    }
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+#pragma unroll
+            for (int i = 0; i < KCH / 4; ++i) nxt[i] = __ldg(arow + (ch + 1) * (KCH / 4) + i);
+        }
+        const float* swc = sw + (size_t)ch * KCH * NJ;
+#pragma unroll
+        for (int i = 0; i < KCH / 4; ++i) {
+            const float av[4] = {cur[i].x, cur[i].y, cur[i].z, cur[i].w};
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const float4* w4 = reinterpret_cast<const float4*>(swc + (4 * i + s) * NJ);
+#pragma unroll
+                for (int j = 0; j < NJ / 4; ++j) {
+                    const float4 ww = w4[j];
+                    acc[4 * j] = fmaf(av[s], ww.x, acc[4 * j]);
+                    acc[4 * j + 1] = fmaf(av[s], ww.y, acc[4 * j + 1]);
+                    acc[4 * j + 2] = fmaf(av[s], ww.z, acc[4 * j + 2]);
+                    acc[4 * j + 3] = fmaf(av[s], ww.w, acc[4 * j + 3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < KCH / 4; ++i) cur[i] = nxt[i];
+    }
+    for (uint32_t t4 = 0; t4 < tail / 4; ++t4) {
+        const float4 v = __ldg(arow + nch * (KCH / 4) + t4);
+        const float av[4] = {v.x, v.y, v.z, v.w};
+        for (int s = 0; s < 4; ++s) {
+            const float4* w4 = reinterpret_cast<const float4*>(sw + (size_t)(nch * KCH + 4 * t4 + s) * NJ);
+#pragma unroll
+            for (int j = 0; j < NJ / 4; ++j) {
+                const float4 ww = w4[j];
+                acc[4 * j] = fmaf(av[s], ww.x, acc[4 * j]);
+                acc[4 * j + 1] = fmaf(av[s], ww.y, acc[4 * j + 1]);
+                acc[4 * j + 2] = fmaf(av[s], ww.z, acc[4 * j + 2]);
+                acc[4 * j + 3] = fmaf(av[s], ww.w, acc[4 * j + 3]);
+            }
+        }
+    }
+    float* o = static_cast<float*>(g.out) + row * g.n + j0;
+    const float* b = g.epilogue == 1 ? static_cast<const float*>(g.bias) + j0 : nullptr;
+    const float sc = g.epilogue == 2 ? (float)g.row_scale[row] : 1.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        if (j >= (int)nj) break;
+        float v = acc[j];
+        if (g.epilogue == 1) {
+            v += b[j];
+            v = v > 0.f ? v : 0.f;
+        } else if (g.epilogue == 2) {
+            v *= sc;
+        }
+        acc[j] = v;
+    }
+    if (nj == (uint32_t)NJ && g.n % 4 == 0 && ((uintptr_t)o % 16 == 0)) {
+#pragma unroll
+        for (int j = 0; j < NJ; j += 4)
+            *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (j < (int)nj) o[j] = acc[j];
+    }
+}
+
+// dW partial = A^T B over a CTA's rows, warp-cooperative: lane l owns rows
+// i = l + 32*s (s < PP) of the p-dimension and all QB (padded q) columns;
+// per A row a lane loads PP scalars (the warp reads the row coalesced) and
+// the B row as QB/4 float4 broadcasts.  The CTA's 8 warp partials are summed
+// in warp order in shared memory: one partial per CTA, reduced later in
+// chunk order (deterministic).
+template <int PP, int QB>
+__global__ void __launch_bounds__(256) k6_gemm_tn_warp(const float* __restrict__ a, const float* __restrict__ b,
+                                                       uint32_t m, uint32_t p, uint32_t q, uint32_t rows_per_cta,
+                                                       float* __restrict__ part) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* red = reinterpret_cast<float*>(smem_raw);  // [8][p*q]
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x / 32;
+    const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_cta;
+    const uint64_t r_end = r_begin + rows_per_cta < m ? r_begin + rows_per_cta : m;
+    float acc[PP][QB];
+#pragma unroll
+    for (int s = 0; s < PP; ++s)
+#pragma unroll
+        for (int j = 0; j < QB; ++j) acc[s][j] = 0.f;
+    const bool bvec = (q % 4 == 0) && ((uintptr_t)b % 16 == 0);
+#pragma unroll 4
+    for (uint64_t r = r_begin + wid; r < r_end; r += 8) {
+        float av[PP];
+#pragma unroll
+        for (int s = 0; s < PP; ++s) {
+            const uint32_t i = lane + 32 * s;
+            av[s] = i < p ? __ldg(a + r * p + i) : 0.f;
+        }
+        float bv[QB];
+        if (bvec) {
+#pragma unroll
+            for (int j = 0; j < QB; j += 4) {
+                const float4 t = j < (int)q ? __ldg(reinterpret_cast<const float4*>(b + r * q + j))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                bv[j] = t.x;
+                bv[j + 1] = t.y;
+                bv[j + 2] = t.z;
+                bv[j + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < QB; ++j) bv[j] = j < (int)q ? __ldg(b + r * q + j) : 0.f;
+        }
+#pragma unroll
+        for (int s = 0; s < PP; ++s)
+#pragma unroll
+            for (int j = 0; j < QB; ++j) acc[s][j] = fmaf(av[s], bv[j], acc[s][j]);
+    }
+    // warp partials -> shared memory -> sum over warps in order
+#pragma unroll
+    for (int s = 0; s < PP; ++s) {
+        const uint32_t i = lane + 32 * s;
+        if (i < p)
+#pragma unroll
+            for (int j = 0; j < QB; ++j)
+                if (j < (int)q) red[(size_t)wid * p * q + i * q + j] = acc[s][j];
+    }
+    __syncthreads();
+    const uint32_t total = p * q;
+    for (uint32_t o = threadIdx.x; o < total; o += blockDim.x) {
+        float sum = 0.f;
+        for (uint32_t w2 = 0; w2 < 8; ++w2) sum += red[(size_t)w2 * total + o];
+        part[(size_t)blockIdx.x * total + o] = sum;
+    }
+}
+
+// Partial C = A^T B over a chunk of rows, 4x4 register blocks per thread:
+// thread (ti, tj) owns C[4ti..4ti+3][4tj..4tj+3]; rows staged 32 at a time
+// (float4, 16-byte aligned row strides).  Requires p, q multiples of 4 and
+// (p/4)(q/4) <= 1024.
+constexpr int TN4_ROWS = 32;
+
+__global__ void k6_gemm_tn4(const float* __restrict__ a, const float* __restrict__ b, uint32_t m, uint32_t p,
+                            uint32_t q, uint32_t rows_per_chunk, float* __restrict__ part) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float4* sa = reinterpret_cast<float4*>(smem_raw);  // [TN4_ROWS][p/4]
+    float4* sb = sa + (size_t)TN4_ROWS * (p / 4);     // [TN4_ROWS][q/4]
+    const uint32_t p4 = p / 4, q4 = q / 4;
+    const uint32_t ti = threadIdx.x / q4, tj = threadIdx.x % q4;
+    const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_chunk;
+    const uint64_t r_end = r_begin + rows_per_chunk < m ? r_begin + rows_per_chunk : m;
+    float acc[4][4] = {};
+    const float4* a4 = reinterpret_cast<const float4*>(a);
+    const float4* b4 = reinterpret_cast<const float4*>(b);
+    for (uint64_t r0 = r_begin; r0 < r_end; r0 += TN4_ROWS) {
+        const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)TN4_ROWS ? r_end - r0 : (uint64_t)TN4_ROWS);
+#pragma unroll 8
+        for (uint32_t e = threadIdx.x; e < TN4_ROWS * p4; e += blockDim.x) {
+            const uint32_t r = e / p4;
+            sa[e] = r < nr ? __ldg(a4 + (r0 + r) * p4 + e % p4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll 4
+        for (uint32_t e = threadIdx.x; e < TN4_ROWS * q4; e += blockDim.x) {
+            const uint32_t r = e / q4;
+            sb[e] = r < nr ? __ldg(b4 + (r0 + r) * q4 + e % q4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        if (ti < p4) {
+            for (uint32_t r = 0; r < nr; ++r) {
+                const float4 x = sa[r * p4 + ti], y = sb[r * q4 + tj];
+                const float xa[4] = {x.x, x.y, x.z, x.w}, ya[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xa[i], ya[j], acc[i][j]);
+            }
+        }
+        __syncthreads();
+    }
+    if (ti >= p4) return;
+    float* out = part + (size_t)blockIdx.x * p * q;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<float4*>(out + (size_t)(4 * ti + i) * q + 4 * tj) =
+            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+}
+
+// Deterministic chunk reduction with a warp per output: lanes take chunks
+// lane, lane+32, ... and a fixed shuffle tree combines them.
+__global__ void k6_reduce_chunks_warp(const float* __restrict__ part, uint32_t chunks, uint32_t total,
+                                      float* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t o = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; o < total; o += warps) {
+        float s = 0.f;
+        for (uint32_t c = lane; c < chunks; c += 32) s += part[(size_t)c * total + o];
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) out[o] = s;
+    }
+}
+
 template <class T>
 void launch_gemm(gnna_ctx* ctx, const GemmArgs& g, bool exact) {
     if (g.m == 0 || g.n == 0) return;
+    if constexpr (std::is_same<T, float>::value) {
+        if (!exact) {
+            const uint32_t nj = g.n <= 4 ? 4 : g.n <= 8 ? 8 : g.n <= 16 ? 16 : 32;
+            dim3 grid((g.m + ROWS - 1) / ROWS, (g.n + nj - 1) / nj);
+            const size_t wbytes = (size_t)g.k * nj * 4;
+            if (g.k % 4 == 0 && ((uintptr_t)g.a % 16 == 0) && wbytes <= 64 * 1024) {
+                auto launch = [&](auto kern) {
+                    if (wbytes > 48 * 1024)
+                        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes));
+                    kern<<<grid, 128, wbytes, ctx->stream>>>(g);
+                };
+                switch (nj) {
+                    case 4: launch(k6_gemm_rows<4>); break;
+                    case 8: launch(k6_gemm_rows<8>); break;
+                    case 16: launch(k6_gemm_rows<16>); break;
+                    default: launch(k6_gemm_rows<32>); break;
+                }
+                gnna::launched(ctx, "k6_gemm_rows");
+                return;
+            }
+            switch (nj) {
+                case 4: k6_gemm_f32<4><<<grid, ROWS, 0, ctx->stream>>>(g); break;
+                case 8: k6_gemm_f32<8><<<grid, ROWS, 0, ctx->stream>>>(g); break;
+                case 16: k6_gemm_f32<16><<<grid, ROWS, 0, ctx->stream>>>(g); break;
+                default: k6_gemm_f32<32><<<grid, ROWS, 0, ctx->stream>>>(g); break;
+            }
+            gnna::launched(ctx, "k6_gemm_f32");
+            return;
+        }
+    }
     dim3 grid((g.m + ROWS - 1) / ROWS, (g.n + NJ - 1) / NJ);
     if (exact)
         k6_gemm<T, true><<<grid, ROWS, 0, ctx->stream>>>(g);
@@ -205,6 +555,58 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
     if (m == 0) {
         GNNA_CUDA(cudaMemsetAsync(out, 0, (size_t)total * sizeof(T), ctx->stream));
         return;
+    }
+    if constexpr (std::is_same<T, float>::value) {
+        if (p <= 128 && q <= 32) {
+            const uint32_t pp = (p + 31) / 32;
+            const uint32_t qb = q <= 4 ? 4 : q <= 8 ? 8 : q <= 16 ? 16 : 32;
+            uint32_t ctas = std::max<uint32_t>(1, std::min<uint32_t>(2 * ctx->num_sms, (m + 255) / 256));
+            const uint32_t rpc = (m + ctas - 1) / ctas;
+            ctas = (m + rpc - 1) / rpc;
+            DevBuf<float> part((size_t)ctas * total, ctx->stream);
+            const size_t smem = (size_t)8 * total * sizeof(float);
+            auto launch = [&](auto kern) {
+                if (smem > 48 * 1024)
+                    GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                kern<<<ctas, 256, smem, ctx->stream>>>(a, b, m, p, q, rpc, part.get());
+            };
+#define GNNA_TNW(PP)                                           \
+    switch (qb) {                                              \
+        case 4: launch(k6_gemm_tn_warp<PP, 4>); break;         \
+        case 8: launch(k6_gemm_tn_warp<PP, 8>); break;         \
+        case 16: launch(k6_gemm_tn_warp<PP, 16>); break;       \
+        default: launch(k6_gemm_tn_warp<PP, 32>); break;       \
+    }
+            switch (pp) {
+                case 1: GNNA_TNW(1) break;
+                case 2: GNNA_TNW(2) break;
+                case 3: GNNA_TNW(3) break;
+                default: GNNA_TNW(4) break;
+            }
+#undef GNNA_TNW
+            gnna::launched(ctx, "k6_gemm_tn_warp");
+            k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
+                part.get(), ctas, total, out);
+            gnna::launched(ctx, "k6_reduce_chunks_warp");
+            return;
+        }
+        const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)out % 16 == 0);
+        if (aligned && p % 4 == 0 && q % 4 == 0 && (p / 4) * (q / 4) <= 1024) {
+            const uint32_t threads = ((p / 4) * (q / 4) + 31) / 32 * 32;
+            uint32_t chunks = std::max<uint32_t>(1, std::min<uint32_t>(8 * ctx->num_sms, (m + 63) / 64));
+            const uint32_t rpc = (m + chunks - 1) / chunks;
+            chunks = (m + rpc - 1) / rpc;
+            DevBuf<float> part((size_t)chunks * total, ctx->stream);
+            const size_t smem = (size_t)TN4_ROWS * (p + q) * sizeof(float);
+            if (smem > 48 * 1024)
+                GNNA_CUDA(cudaFuncSetAttribute(k6_gemm_tn4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k6_gemm_tn4<<<chunks, threads, smem, ctx->stream>>>(a, b, m, p, q, rpc, part.get());
+            gnna::launched(ctx, "k6_gemm_tn4");
+            k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
+                part.get(), chunks, total, out);
+            gnna::launched(ctx, "k6_reduce_chunks_warp");
+            return;
+        }
     }
     const uint32_t tiles = (total + TN_OUT - 1) / TN_OUT;
     uint32_t chunks = std::max<uint32_t>(1, std::min<uint32_t>(4 * ctx->num_sms / tiles + 1, (m + 255) / 256));
