@@ -207,6 +207,22 @@ GNNA_API gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const ui
                                      uint64_t line_bytes, uint64_t cache_capacity,
                                      uint64_t cache_line, gnna_cost* cost);
 
+/* A stream of host-buffer aggregations (one per batch: its own CSR row
+ * range and features), pipelined: batch i+1's uploads overlap batch i's
+ * planning + K3 and batch i-1's download (two device buffer sets, separate
+ * copy streams; PCIe is full duplex).  Same results as calling
+ * gnna_aggregate_host_rows per batch.  Host buffers should be pinned. */
+typedef struct {
+    const uint64_t* h_row_ptr;
+    const uint32_t* h_col;
+    uint32_t n, row_begin, row_end;
+    const void* h_x;
+    void* h_y;  /* (row_end - row_begin) x dim */
+} gnna_host_batch;
+GNNA_API gnna_status gnna_aggregate_host_stream(gnna_ctx* ctx, int dtype, const gnna_params* p, int strategy,
+                                       int dim_mode, const gnna_host_batch* batches,
+                                       uint32_t num_batches);
+
 /* -------------------------------------------------------- GCN / GIN --- */
 /* engine.cpp:340-353: norm[v] = 1/sqrt(max(deg'(v),1)) (f64), deg' counts an
  * implicit self loop when add_self_loops and v has none; d_self (u8, may be

@@ -77,6 +77,12 @@ class AggOpts(C.Structure):
                 ("row_scale", C.c_void_p), ("relu", C.c_int), ("mask", C.c_void_p)]
 
 
+class HostBatch(C.Structure):
+    """gnna_host_batch (include/gnna.h)."""
+    _fields_ = [("h_row_ptr", C.c_void_p), ("h_col", C.c_void_p), ("n", C.c_uint32), ("row_begin", C.c_uint32),
+                ("row_end", C.c_uint32), ("h_x", C.c_void_p), ("h_y", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -270,6 +276,17 @@ class Context:
                                                     C.c_int(strategy), C.c_int(dim_mode), _ptr(x), _ptr(out),
                                                     C.c_uint64(128), C.c_uint64(0), C.c_uint64(0), None))
         return out
+
+    def aggregate_host_stream(self, p: Params, batches, strategy=WARP_SHARED, dim_mode=DIM_CYCLIC):
+        """gnna_aggregate_host_stream: batches = [(row_ptr, col, x, r0, r1, out)] of host (pinned) tensors,
+        processed with uploads/compute/downloads of consecutive batches overlapped."""
+        arr = (HostBatch * len(batches))()
+        dt = None
+        for i, (rp, col, x, r0, r1, out) in enumerate(batches):
+            arr[i] = HostBatch(_ptr(rp).value, _ptr(col).value, rp.numel() - 1, r0, r1, _ptr(x).value, _ptr(out).value)
+            dt = _dtype_code(x)
+        self._check(self.L.gnna_aggregate_host_stream(self.h, C.c_int(dt), C.byref(p), C.c_int(strategy),
+                                                      C.c_int(dim_mode), arr, C.c_uint32(len(batches))))
 
     # ------------------------------------------------------- layers (K5/K6)
     def gemm(self, a, w, bias=None, epilogue=0, row_scale=None, out=None):

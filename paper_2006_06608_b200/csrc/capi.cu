@@ -1,4 +1,5 @@
 // Context lifecycle and the host-buffer end-to-end entry of include/gnna.h.
+#include <algorithm>
 #include <cstring>
 
 #include "gnna_common.cuh"
@@ -138,6 +139,106 @@ gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const uint64_t* h
             throw;
         }
         gnna_plan_destroy(plan);
+    });
+}
+
+gnna_status gnna_aggregate_host_stream(gnna_ctx* ctx, int dtype, const gnna_params* p, int strategy, int dim_mode,
+                                       const gnna_host_batch* batches, uint32_t num_batches) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        gnna::validate_params(p);
+        if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        if (!num_batches) return;
+        if (!batches) gnna::raise(GNNA_ERR_DOMAIN, "null batches");
+        const size_t elem = dtype == GNNA_F32 ? 4 : 8;
+        // capacity of one device buffer set = max over the batches
+        uint64_t max_rows = 0, max_nnz = 0, max_x = 0;
+        for (uint32_t i = 0; i < num_batches; ++i) {
+            const gnna_host_batch& b = batches[i];
+            if (b.row_begin > b.row_end || b.row_end > b.n) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_host: bad row range");
+            max_rows = std::max<uint64_t>(max_rows, b.row_end - b.row_begin);
+            max_nnz = std::max<uint64_t>(max_nnz, b.h_row_ptr[b.row_end] - b.h_row_ptr[b.row_begin]);
+            max_x = std::max<uint64_t>(max_x, (uint64_t)b.n * p->dim * elem);
+        }
+        cudaStream_t cs = ctx->stream, up = nullptr, down = nullptr;
+        GNNA_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+        GNNA_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+        struct Slot {
+            gnna::DevBuf<uint64_t> rp;
+            gnna::DevBuf<uint32_t> col;
+            gnna::DevBuf<uint8_t> x, y;
+            cudaEvent_t uploaded = nullptr, computed = nullptr, downloaded = nullptr;
+        } slot[2];
+        auto cleanup = [&] {
+            cudaStreamSynchronize(up);
+            cudaStreamSynchronize(down);
+            cudaStreamSynchronize(cs);
+            for (auto& s : slot) {
+                if (s.uploaded) cudaEventDestroy(s.uploaded);
+                if (s.computed) cudaEventDestroy(s.computed);
+                if (s.downloaded) cudaEventDestroy(s.downloaded);
+            }
+            cudaStreamDestroy(up);
+            cudaStreamDestroy(down);
+        };
+        try {
+            for (auto& s : slot) {
+                s.rp = gnna::DevBuf<uint64_t>(max_rows + 1, cs);
+                s.col = gnna::DevBuf<uint32_t>(max_nnz ? max_nnz : 1, cs);
+                s.x = gnna::DevBuf<uint8_t>(max_x ? max_x : 1, cs);
+                s.y = gnna::DevBuf<uint8_t>(max_rows * p->dim * elem + 1, cs);
+                GNNA_CUDA(cudaEventCreateWithFlags(&s.uploaded, cudaEventDisableTiming));
+                GNNA_CUDA(cudaEventCreateWithFlags(&s.computed, cudaEventDisableTiming));
+                GNNA_CUDA(cudaEventCreateWithFlags(&s.downloaded, cudaEventDisableTiming));
+                // start "free": nothing to wait for
+                GNNA_CUDA(cudaEventRecord(s.computed, cs));
+                GNNA_CUDA(cudaEventRecord(s.downloaded, cs));
+            }
+            GNNA_CUDA(cudaStreamSynchronize(cs));  // buffers allocated before the copy streams use them
+            auto upload = [&](uint32_t i) {
+                const gnna_host_batch& b = batches[i];
+                Slot& s = slot[i & 1];
+                const uint32_t rows = b.row_end - b.row_begin;
+                const uint64_t e0 = b.h_row_ptr[b.row_begin], nnz = b.h_row_ptr[b.row_end] - e0;
+                GNNA_CUDA(cudaStreamWaitEvent(up, s.computed, 0));  // slot's previous batch done reading
+                GNNA_CUDA(cudaMemcpyAsync(s.rp.get(), b.h_row_ptr + b.row_begin, ((size_t)rows + 1) * 8,
+                                          cudaMemcpyHostToDevice, up));
+                if (nnz) GNNA_CUDA(cudaMemcpyAsync(s.col.get(), b.h_col + e0, nnz * 4, cudaMemcpyHostToDevice, up));
+                const size_t xb = (size_t)b.n * p->dim * elem;
+                if (xb) GNNA_CUDA(cudaMemcpyAsync(s.x.get(), b.h_x, xb, cudaMemcpyHostToDevice, up));
+                GNNA_CUDA(cudaEventRecord(s.uploaded, up));
+            };
+            upload(0);
+            for (uint32_t i = 0; i < num_batches; ++i) {
+                const gnna_host_batch& b = batches[i];
+                Slot& s = slot[i & 1];
+                if (i + 1 < num_batches) upload(i + 1);  // keep the H2D engine busy
+                const uint32_t rows = b.row_end - b.row_begin;
+                const uint64_t e0 = b.h_row_ptr[b.row_begin];
+                GNNA_CUDA(cudaStreamWaitEvent(cs, s.uploaded, 0));
+                GNNA_CUDA(cudaStreamWaitEvent(cs, s.downloaded, 0));  // y slot free
+                if (e0) gnna::rebase_u64(ctx, s.rp.get(), (uint64_t)rows + 1, e0);
+                gnna_plan* plan = nullptr;
+                gnna_status st = gnna_plan_create(ctx, s.rp.get(), s.col.get(), rows, 0, rows, p, strategy, &plan);
+                if (st != GNNA_OK) gnna::raise(st, ctx->err);
+                try {
+                    gnna::aggregate_plan(ctx, plan, dtype, dim_mode, s.x.get(), s.y.get(), 0, nullptr, 0.0);
+                } catch (...) {
+                    gnna_plan_destroy(plan);
+                    throw;
+                }
+                GNNA_CUDA(cudaEventRecord(s.computed, cs));
+                gnna_plan_destroy(plan);  // stream-ordered frees
+                GNNA_CUDA(cudaStreamWaitEvent(down, s.computed, 0));
+                const size_t yb = (size_t)rows * p->dim * elem;
+                if (yb) GNNA_CUDA(cudaMemcpyAsync(b.h_y, s.y.get(), yb, cudaMemcpyDeviceToHost, down));
+                GNNA_CUDA(cudaEventRecord(s.downloaded, down));
+            }
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
     });
 }
 

@@ -183,3 +183,32 @@ def test_power_law_hubs_f32(ctx, orc):
             assert np.array_equal(got, want), (kw, s)
             got32 = plan.aggregate(dx.float()).cpu().numpy()
             assert (np.abs(got32 - want) <= 1e-5 * np.abs(want)).all()
+
+
+def test_host_stream_matches_per_batch(ctx, orc):
+    """gnna_aggregate_host_stream: pipelined batches (different graphs, row
+    ranges and sizes) give exactly the per-batch results."""
+    import torch
+    rng = np.random.default_rng(31)
+    p = P(ngs=8, dw=32, tpb=128, dim=16)
+    batches, wants = [], []
+    for t in range(5):
+        n = int(rng.integers(50, 3000))
+        rp, col, _ = random_graph(rng, n, 5 * n)
+        r0 = int(rng.integers(0, n // 2))
+        r1 = int(rng.integers(r0, n + 1))
+        x = rng.random((n, 16))
+        # a shard's schedule starts at its first row: the reference result is
+        # aggregate_scheduled on the row-slice graph (rows x n CSR, full x)
+        sub_rp = (rp[r0:r1 + 1] - rp[r0]).astype(np.uint64)
+        sub_col = col[rp[r0]:rp[r1]].copy()
+        want, _ = orc.aggregate_scheduled(sub_rp, sub_col, x, p.tolist(), 2, 1)
+        want = np.concatenate([np.zeros((r0, 16)), want])
+        out = torch.empty((r1 - r0, 16), dtype=torch.float64).pin_memory()
+        batches.append((torch.from_numpy(rp.view(np.int64)).pin_memory(),
+                        torch.from_numpy(col.view(np.int32)).pin_memory(),
+                        torch.from_numpy(x).pin_memory(), r0, r1, out))
+        wants.append(want[r0:r1])
+    ctx.aggregate_host_stream(p, batches)
+    for (_, _, _, _, _, out), want in zip(batches, wants):
+        assert np.array_equal(out.numpy(), want)
