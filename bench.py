@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-nodes", type=int, default=0, help="CPU-baseline sample size (nodes)")
     ap.add_argument("--flush-l2", action="store_true", help="force an L2 flush between steps")
+    ap.add_argument("--evaluator", default="b200", choices=["b200", "reference"],
+                    help="parameter choice: B200 cost model (default) or the reference's decider rules")
     return ap.parse_args()
 
 
@@ -224,8 +226,10 @@ def run_ours(args):
     gen_s = time.time() - t0
 
     # Parameters: the performance evaluator with the B200 profile, unless overridden.
-    mi = ctx.model_inputs(rp, cfg.dim, b200=True)
-    p = ctx.auto_params(mi)
+    if args.evaluator == "reference":
+        p = ctx.auto_params(ctx.model_inputs(rp, cfg.dim, b200=True))  # decider.cpp rules
+    else:
+        p, _ = ctx.b200_params(rp, cfg.dim)  # B200 cost model (gnna_b200_auto_params)
     if args.ngs:
         p.ngs = args.ngs
     if args.dw:

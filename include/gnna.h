@@ -347,6 +347,12 @@ GNNA_API gnna_status gnna_search_params(const gnna_model_inputs* in, uint32_t it
 /* B200 profile of the evaluator: 148 SMs, 227 KiB smem per block, runtime
  * L2/HBM figures.  Fills `in` device fields from the live device. */
 GNNA_API gnna_status gnna_b200_profile(gnna_ctx* ctx, gnna_model_inputs* in);
+/* B200 evaluator (north-star subsystem 3): picks ngs from a calibrated
+ * cost model T(ngs) = max(B_alg/BW + G(ngs)*c_unit, min(ngs, max_degree)*c_edge)
+ * with G = n + nnz/ngs; tpb = 512; dw = select_dw(dim).  hbm_gbs <= 0 uses
+ * 6553 (MEASURED_PEAKS.json).  *est_us (may be NULL) = the model's K3 time. */
+GNNA_API gnna_status gnna_b200_auto_params(const gnna_model_inputs* in, uint64_t max_degree, double hbm_gbs,
+                                  gnna_params* out, double* est_us);
 /* Measured-latency tuner: times gnna_aggregate (F32) on the live graph for
  * every (ngs, dw, tpb) in the grid and returns the fastest (K3 sweep). */
 GNNA_API gnna_status gnna_tune_params(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,

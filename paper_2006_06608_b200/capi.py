@@ -98,6 +98,7 @@ def lib():
         _lib.gnna_get_stream.restype = C.c_void_p
         _lib.gnna_alpha_from_degrees.restype = C.c_double
         _lib.gnna_alpha_from_degrees.argtypes = [C.c_double, C.c_double]
+        _lib.gnna_decider_last_error.restype = C.c_char_p
     return _lib
 
 
@@ -416,6 +417,24 @@ class Context:
         return best, ms.value
 
     # ------------------------------------------------------------- decider
+    def b200_params(self, row_ptr, dim, hbm_gbs=0.0):
+        """The B200 evaluator (gnna_b200_auto_params) on this graph: (Params, model K3 microseconds)."""
+        mi = self.model_inputs(row_ptr, dim, b200=True)
+        _, maxd, _ = self.degree_stats(row_ptr)
+        if not hbm_gbs:
+            try:
+                import json
+                hbm_gbs = float(json.load(open(os.path.join(os.path.dirname(HERE), "MEASURED_PEAKS.json")))["hbm_gbs"])
+            except Exception:
+                hbm_gbs = 0.0
+        p = Params()
+        est = C.c_double()
+        rc = self.L.gnna_b200_auto_params(C.byref(mi), C.c_uint64(maxd), C.c_double(hbm_gbs), C.byref(p),
+                                          C.byref(est))
+        if rc:
+            raise DomainError(rc, self.L.gnna_decider_last_error().decode())
+        return p, est.value
+
     def auto_params(self, inputs: ModelInputs) -> Params:
         p = Params()
         rc = self.L.gnna_auto_params(C.byref(inputs), C.byref(p))

@@ -162,8 +162,11 @@ struct TransientPlan {
         gnna_model_inputs mi{};
         check(ctx, gnna_model_inputs_from_graph(ctx, rp, n, dim, &mi));
         check(ctx, gnna_b200_profile(ctx, &mi));
+        double avg = 0, sd = 0;
+        uint64_t maxd = 0;
+        check(ctx, gnna_degree_stats(ctx, rp, n, &avg, &maxd, &sd));
         gnna_params prm{};
-        if (gnna_auto_params(&mi, &prm) != GNNA_OK) prm = gnna_params{16, 32, 128, 32, dim};
+        if (gnna_b200_auto_params(&mi, maxd, 0.0, &prm, nullptr) != GNNA_OK) prm = gnna_params{256, 32, 512, 32, dim};
         prm.dim = dim;
         check(ctx, gnna_plan_create(ctx, rp, col, n, 0, n, &prm, GNNA_WARP_SHARED, &p));
     }

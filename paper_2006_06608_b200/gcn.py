@@ -33,7 +33,7 @@ class GCN2:
         self.dims = (in_dim, hidden, out_dim)
         dev = row_ptr.device
         if params is None:
-            params = ctx.auto_params(ctx.model_inputs(row_ptr, min(hidden, in_dim), b200=True))
+            params, _ = ctx.b200_params(row_ptr, min(hidden, in_dim))
         self.params = params
         # one schedule (K1 units + K2 Algorithm-1 plan) for every aggregation of the step
         self.plan = ctx.plan(row_ptr, col, params, WARP_SHARED)

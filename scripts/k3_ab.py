@@ -46,6 +46,8 @@ def main():
         for ps in args.params.split(","):
             if ps == "auto":
                 p = ctx.auto_params(ctx.model_inputs(rp, cfg.dim, b200=True))
+            elif ps == "b200":
+                p, _ = ctx.b200_params(rp, cfg.dim)
             else:
                 g, d, t = (int(v) for v in ps.split("/"))
                 p = Params.make(ngs=g, dw=d, tpb=t, dim=cfg.dim)

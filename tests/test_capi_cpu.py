@@ -220,3 +220,28 @@ def test_row_sharded_allgather_gloo_world2(tmp_path):
             break
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert r.stdout.count("ok") == 2  # one per rank (the two ranks' lines may interleave)
+
+
+def test_b200_evaluator_choices():
+    """The B200 cost model (gnna_b200_auto_params) reproduces the r01 sweep's
+    optima: mid-size units on C3 (hub tail vs unit overhead), big units on
+    C5, tpb 512, dw from the reference's Eq. 6 rule."""
+    import ctypes as C
+    from paper_2006_06608_b200.capi import ModelInputs, Params, lib
+    L = lib()
+
+    def pick(n, e, dim, maxd):
+        mi = ModelInputs.make(num_nodes=n, num_edges=e, dim=dim, avg_degree=e / n)
+        p, est = Params(), C.c_double()
+        assert L.gnna_b200_auto_params(C.byref(mi), C.c_uint64(maxd), C.c_double(6553.0), C.byref(p),
+                                       C.byref(est)) == 0
+        return p, est.value
+
+    p3, t3 = pick(410236, 4885672, 16, 10000)     # C3 shape: measured optimum ngs 256
+    assert 128 <= p3.ngs <= 512 and p3.tpb == 512 and p3.dw == 16
+    assert 40 < t3 < 120                            # microseconds (measured best 66)
+    p5, t5 = pick(10_000_000, 200_224_114, 128, 160995)  # C5: measured optimum ngs 1024
+    assert p5.ngs >= 512 and p5.dw == 32
+    assert 10_000 < t5 < 25_000
+    mi0 = ModelInputs.make(dim=0)
+    assert L.gnna_b200_auto_params(C.byref(mi0), C.c_uint64(1), C.c_double(0.0), C.byref(Params()), None) == 1
