@@ -114,6 +114,16 @@ class Clocks:
                 "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
 
 
+def ncu_traffic(workload):
+    """DRAM bytes per launch of K3 from the committed ncu --set full capture
+    (profiles/ncu_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[workload]
+        return d["dram_bytes_per_launch"], d["source"]
+    except Exception:
+        return None, None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -320,6 +330,7 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
+    traffic, traffic_src = ncu_traffic(args.workload) if world == 1 else (None, None)
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -332,8 +343,8 @@ def run_ours(args):
                        "plan": plan.info(), "graph_build_s": round(gen_s, 3), "plan_build_s": round(plan_s, 3),
                        "max_degree": int(np.diff(rp_host).max())},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "k3_aggregate (+k3b_fixup)", "kernel_ms": t_agg,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src, "kernel": "k3_aggregate (+k3b_fixup)", "kernel_ms": t_agg,
                          "algorithmic_bytes_per_launch": balg_rank},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -1,4 +1,5 @@
-# Round measurement: tests, bench (C5 default), launch list, ncu --set full of K3 (C5 and C3), sweep
+# Round measurement: tests, bench (C5 default), launch list, ncu --set full of K3 (C5 and C3), sweep.
+# ncu reports are reduced to CSV on the box (gpurun_out/ must stay < 64 MiB).
 set -x
 R=${1:-r01}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
@@ -7,6 +8,11 @@ timeout 1800 python -m pytest tests -m gpu -q --timeout 900 2>&1 | tail -4
 timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err; tail -3 gpurun_out/bench_$R.err
 cat gpurun_out/bench_$R.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu1 $?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3_aggregate -s 2 -c 1 -o gpurun_out/k3_c5_$R python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu2 $?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3_aggregate -s 2 -c 1 -o gpurun_out/k3_c3_$R python bench.py --workload c3 --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu3 $?
+for w in c5 c3; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k3_aggregate -s 2 -c 1 -o /tmp/k3_${w}_$R python bench.py --workload $w --steps 2 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1; echo ncu_$w $?
+  ncu -i /tmp/k3_${w}_$R.ncu-rep --page raw --csv > gpurun_out/k3_${w}_${R}_raw.csv 2>/dev/null
+  ncu -i /tmp/k3_${w}_$R.ncu-rep --page source --csv > gpurun_out/k3_${w}_${R}_source.csv 2>/dev/null
+done
 for w in c1 c2 c3 c4; do timeout 600 python bench.py --workload $w --steps 20 --warmup 5 --no-e2e 2>/dev/null | tail -1; done > gpurun_out/sweep_$R.jsonl
+timeout 600 python bench.py --workload c3train --steps 20 --warmup 5 2>/dev/null | tail -1 > gpurun_out/c3train_$R.json
+du -sh gpurun_out
