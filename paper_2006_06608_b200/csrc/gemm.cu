@@ -16,6 +16,7 @@
 // gemm_tn (dW = A^T B, a reduction over all rows) is split over row chunks
 // with per-chunk partials summed in chunk order: deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "gnna_common.cuh"
@@ -375,6 +376,123 @@ __global__ void __launch_bounds__(128) k6_gemm_rows(GemmArgs g) {
     }
 }
 
+// X·W, software-pipelined: 256 rows per CTA (one output row per thread), A
+// streamed in 16-column chunks through a double-buffered shared tile (row
+// stride 17: conflict-free column reads), the next chunk's four float4 loads
+// per thread in flight while the current chunk is consumed, W resident in
+// shared memory for the whole kernel (float4 broadcasts).  One barrier per
+// chunk.  Requires k % 4 == 0 and a 16-byte aligned A.
+constexpr int PR = 256;  // rows per CTA
+constexpr int PK = 16;   // k chunk
+
+template <int NJ>
+__global__ void __launch_bounds__(PR) k6_gemm_pipe(GemmArgs g) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* sw = reinterpret_cast<float*>(smem_raw);                 // [k][NJ]
+    float (*sa)[PR][PK + 1] = reinterpret_cast<float (*)[PR][PK + 1]>(sw + (size_t)g.k * NJ);  // [2][PR][PK+1]
+    const float* __restrict__ w = static_cast<const float*>(g.w);
+    const float* __restrict__ a = static_cast<const float*>(g.a);
+    const uint32_t j0 = blockIdx.y * NJ;
+    const uint32_t nj = g.n - j0 < (uint32_t)NJ ? g.n - j0 : (uint32_t)NJ;
+    const uint32_t t = threadIdx.x;
+    const uint64_t row0 = (uint64_t)blockIdx.x * PR;
+    for (uint32_t e = t; e < g.k * NJ; e += PR) {
+        const uint32_t r = e / NJ, c = e % NJ;
+        sw[e] = c < nj ? __ldg(w + (uint64_t)r * g.n + j0 + c) : 0.f;
+    }
+    // thread t stages float4 #(t + i*PR) of the [PR][PK] chunk: row (t+i*PR)/4, col4 (t%4)
+    constexpr int LPT = PR * PK / 4 / PR;  // float4 loads per thread per chunk (4)
+    float4 v[LPT];
+    auto load = [&](uint32_t k0) {
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) {
+            const uint32_t e = t + i * PR;
+            const uint32_t r = e / (PK / 4), c4 = e % (PK / 4);
+            const uint64_t gr = row0 + r;
+            const uint32_t kk = k0 + c4 * 4;
+            v[i] = (gr < g.m && kk < g.k) ? __ldg(reinterpret_cast<const float4*>(a + gr * g.k + kk))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int i = 0; i < LPT; ++i) {
+            const uint32_t e = t + i * PR;
+            const uint32_t r = e / (PK / 4), c = (e % (PK / 4)) * 4;
+            sa[buf][r][c] = v[i].x;
+            sa[buf][r][c + 1] = v[i].y;
+            sa[buf][r][c + 2] = v[i].z;
+            sa[buf][r][c + 3] = v[i].w;
+        }
+    };
+    float acc[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+    const uint32_t nch = (g.k + PK - 1) / PK;
+    load(0);
+    store(0);
+    __syncthreads();
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+        const int buf = ch & 1;
+        if (ch + 1 < nch) load((ch + 1) * PK);  // in flight during the FMAs below
+        const float* swc = sw + (size_t)ch * PK * NJ;
+        const uint32_t kc = g.k - ch * PK < (uint32_t)PK ? g.k - ch * PK : (uint32_t)PK;
+        if (kc == (uint32_t)PK) {
+#pragma unroll
+            for (int kk = 0; kk < PK; ++kk) {
+                const float av = sa[buf][t][kk];
+#pragma unroll
+                for (int j = 0; j < NJ; j += 4) {
+                    const float4 ww = *reinterpret_cast<const float4*>(swc + kk * NJ + j);
+                    acc[j] = fmaf(av, ww.x, acc[j]);
+                    acc[j + 1] = fmaf(av, ww.y, acc[j + 1]);
+                    acc[j + 2] = fmaf(av, ww.z, acc[j + 2]);
+                    acc[j + 3] = fmaf(av, ww.w, acc[j + 3]);
+                }
+            }
+        } else {
+            for (uint32_t kk = 0; kk < kc; ++kk) {
+                const float av = sa[buf][t][kk];
+#pragma unroll
+                for (int j = 0; j < NJ; j += 4) {
+                    const float4 ww = *reinterpret_cast<const float4*>(swc + kk * NJ + j);
+                    acc[j] = fmaf(av, ww.x, acc[j]);
+                    acc[j + 1] = fmaf(av, ww.y, acc[j + 1]);
+                    acc[j + 2] = fmaf(av, ww.z, acc[j + 2]);
+                    acc[j + 3] = fmaf(av, ww.w, acc[j + 3]);
+                }
+            }
+        }
+        if (ch + 1 < nch) store(buf ^ 1);  // the other buffer: last read before the previous barrier
+        __syncthreads();
+    }
+    const uint64_t row = row0 + t;
+    if (row >= g.m) return;
+    float* o = static_cast<float*>(g.out) + row * g.n + j0;
+    const float* bias = g.epilogue == 1 ? static_cast<const float*>(g.bias) + j0 : nullptr;
+    const float sc = g.epilogue == 2 ? (float)g.row_scale[row] : 1.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        float x = acc[j];
+        if (g.epilogue == 1) {
+            x += j < (int)nj ? bias[j] : 0.f;
+            x = x > 0.f ? x : 0.f;
+        } else if (g.epilogue == 2) {
+            x *= sc;
+        }
+        acc[j] = x;
+    }
+    if (nj == (uint32_t)NJ && g.n % 4 == 0 && ((uintptr_t)o % 16 == 0)) {
+#pragma unroll
+        for (int j = 0; j < NJ; j += 4)
+            *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+            if (j < (int)nj) o[j] = acc[j];
+    }
+}
+
 // dW partial = A^T B over a CTA's rows, warp-cooperative: lane l owns rows
 // i = l + 32*s (s < PP) of the p-dimension and all QB (padded q) columns;
 // per A row a lane loads PP scalars (the warp reads the row coalesced) and
@@ -515,6 +633,24 @@ void launch_gemm(gnna_ctx* ctx, const GemmArgs& g, bool exact) {
             const uint32_t nj = g.n <= 4 ? 4 : g.n <= 8 ? 8 : g.n <= 16 ? 16 : 32;
             dim3 grid((g.m + ROWS - 1) / ROWS, (g.n + nj - 1) / nj);
             const size_t wbytes = (size_t)g.k * nj * 4;
+            const size_t pbytes = wbytes + (size_t)2 * PR * (PK + 1) * 4;
+            static const bool use_rows = std::getenv("GNNA_GEMM_ROWS") != nullptr;  // A/B switch
+            if (!use_rows && g.k % 4 == 0 && ((uintptr_t)g.a % 16 == 0) && pbytes <= 200 * 1024) {
+                dim3 pgrid((g.m + PR - 1) / PR, (g.n + nj - 1) / nj);
+                auto launch = [&](auto kern) {
+                    if (pbytes > 48 * 1024)
+                        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes));
+                    kern<<<pgrid, PR, pbytes, ctx->stream>>>(g);
+                };
+                switch (nj) {
+                    case 4: launch(k6_gemm_pipe<4>); break;
+                    case 8: launch(k6_gemm_pipe<8>); break;
+                    case 16: launch(k6_gemm_pipe<16>); break;
+                    default: launch(k6_gemm_pipe<32>); break;
+                }
+                gnna::launched(ctx, "k6_gemm_pipe");
+                return;
+            }
             if (g.k % 4 == 0 && ((uintptr_t)g.a % 16 == 0) && wbytes <= 64 * 1024) {
                 auto launch = [&](auto kern) {
                     if (wbytes > 48 * 1024)
