@@ -183,7 +183,12 @@ def run_reference(args):
     nodes = args.cpu_nodes or default_cpu_nodes(cfg)
     ref, rp, col, x = cpu_sample(cfg, nodes)
     workers = os.cpu_count() or 1
-    params = [args.ngs or 256, args.dw or 32, args.tpb or 128, 32, cfg.dim]
+    # the reference's own evaluator (decider.cpp auto_params) on the sample graph
+    params = [int(v) for v in ref.auto_params(ref.model_inputs(rp, col, cfg.dim))]
+    if args.ngs:
+        params[0] = args.ngs
+    if args.tpb:
+        params[2] = args.tpb
     nnz = int(rp[-1])
     for _ in range(args.warmup):
         time_reference(ref, rp, col, x, params, workers, 1)
@@ -320,10 +325,12 @@ def run_ours(args):
             ref, srp, scol, sx = cpu_sample(cfg, nodes)
             workers = os.cpu_count() or 1
             reps = 2
-            ts = time_reference(ref, srp, scol, sx, [p.ngs, p.dw, p.tpb, 32, cfg.dim], workers, reps)
+            rparams = [int(v) for v in ref.auto_params(ref.model_inputs(srp, scol, cfg.dim))]  # decider.cpp
+            ts = time_reference(ref, srp, scol, sx, rparams, workers, reps)
             snnz = int(srp[-1])
             cpu = {"value": snnz * cfg.dim / ts, "unit": UNIT, "cores": workers, "kind": "reference",
-                   "sample": f"reference aggregate_scheduled (WarpShared, Cyclic, fp64, workers={workers}) on "
+                   "sample": f"reference aggregate_scheduled (WarpShared, Cyclic, fp64, workers={workers}, "
+                             f"its own auto_params {rparams[:3]}) on "
                              f"{cfg.name} generator at n={len(srp) - 1}, nnz={snnz}, d={cfg.dim}; "
                              f"mean of {reps} calls ({ts:.2f} s each)"}
         except Exception as exc:  # the baseline is reported, not required
