@@ -206,6 +206,7 @@ __global__ void k8_replay(ReplayArgs a, uint64_t* __restrict__ gkeys, uint32_t* 
                                 bi = oi;
                             }
                         }
+                        __syncwarp();  // all lanes' stamp reads above precede lane 0's overwrite (WAR)
                         if (lane == 0) {
                             keys[bi] = l;
                             stamp[bi] = clock;

@@ -1,0 +1,68 @@
+"""Small GPU workload exercising every kernel family once, for compute-sanitizer
+(memcheck / racecheck / synccheck).  Exits non-zero on any parity error."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from oracle.cpu import Oracle  # noqa: E402
+from paper_2006_06608_b200.capi import Context, Params  # noqa: E402
+from paper_2006_06608_b200.gcn import GCN2  # noqa: E402
+
+
+def dev(a):
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.dtype == torch.uint64:
+        t = t.view(torch.int64)
+    elif t.dtype == torch.uint32:
+        t = t.view(torch.int32)
+    return t.cuda()
+
+
+def main():
+    orc = Oracle("orc")
+    ctx = Context(0)
+    rng = np.random.default_rng(1)
+    n = 3000
+    w = 1.0 / np.arange(1, n + 1) ** 0.8
+    src = rng.choice(n, size=20000, p=w / w.sum())
+    edges = np.stack([src, rng.integers(0, n, 20000)], 1).astype(np.uint32)
+    rp, col = orc.to_csr(n, edges, True)
+    drp, dcol = dev(rp), dev(col)
+    rp2, col2 = ctx.to_csr(n, dev(edges), True)
+    assert np.array_equal(rp2.cpu().numpy().view(np.uint64), rp)
+    for dim in (16, 64, 130):
+        x = rng.random((n, dim))
+        for s in (0, 1, 2):
+            p = Params.make(ngs=5, dw=8, tpb=128, dim=dim)
+            plan = ctx.plan(drp, dcol, p, s)
+            want, cost = orc.aggregate_scheduled(rp, col, x, p.tolist(), s, 1, cache=(4096, 128))
+            got = plan.aggregate(dev(x)).cpu().numpy()
+            assert np.array_equal(got, want)
+            c = plan.cost(line=128, cache=(4096, 128))
+            assert c.tolist() == cost.tolist()
+            plan.aggregate(dev(x).float())
+    x = rng.random((n, 24))
+    wt = rng.random((24, 8)) - 0.5
+    assert np.array_equal(ctx.gcn_forward(drp, dcol, dev(x), dev(wt), True).cpu().numpy(),
+                          orc.gcn_layer(rp, col, x, wt, True))
+    ctx.gcn_backward(drp, dcol, dev(x).float(), dev(wt).float(), dev(rng.random((n, 8))).float(), True)
+    b = rng.random(8)
+    ctx.gin_backward(drp, dcol, dev(x), 0.1, dev(wt), dev(b), dev(rng.random((n, 8))))
+    com, k = ctx.detect_communities(drp, dcol)
+    c2, k2 = orc.detect_communities(rp, col)
+    assert k == k2 and np.array_equal(com.cpu().numpy().view(np.uint32), c2)
+    o2n, n2o = ctx.build_mapping(com, k)
+    ctx.apply_mapping_csr(drp, dcol, o2n, n2o)
+    m = GCN2(ctx, drp, dcol, 24, 16, 8)
+    m.step(dev(x).float(), dev(rng.random((n, 8))).float())
+    torch.cuda.synchronize()
+    print("sanitize workload ok")
+
+
+if __name__ == "__main__":
+    main()
