@@ -169,8 +169,9 @@ def time_reference(ref, rp, col, x, params, workers, reps):
 
 
 def default_cpu_nodes(cfg):
-    # ~1-3 s per reference call on an 8+ core host
-    return min(cfg.n, {16: 400_000, 64: 150_000, 128: 200_000}.get(cfg.dim, 150_000))
+    # the whole graph for C1-C4; a 1M-node / ~20M-edge sample of C5 (~1-3 s
+    # per reference call on a 16-thread host)
+    return min(cfg.n, 1_000_000)
 
 
 # ------------------------------------------------------------ reference arm
@@ -324,7 +325,7 @@ def run_ours(args):
             nodes = args.cpu_nodes or default_cpu_nodes(cfg)
             ref, srp, scol, sx = cpu_sample(cfg, nodes)
             workers = os.cpu_count() or 1
-            reps = 2
+            reps = 3
             rparams = [int(v) for v in ref.auto_params(ref.model_inputs(srp, scol, cfg.dim))]  # decider.cpp
             ts = time_reference(ref, srp, scol, sx, rparams, workers, reps)
             snnz = int(srp[-1])
