@@ -218,7 +218,12 @@ class Context:
         n = len(row_ptr) - 1
         if out is None:
             out = np.empty_like(x)
-        dt = F32 if x.dtype in (np.float32,) or str(x.dtype) == "torch.float32" else F64
+        if isinstance(x, np.ndarray):
+            if x.dtype not in (np.float32, np.float64):
+                raise TypeError(f"unsupported feature dtype {x.dtype}")
+            dt = F32 if x.dtype == np.float32 else F64
+        else:
+            dt = _dtype_code(x)
         cost = Cost()
         cap, cl = cache if cache else (0, 0)
         self._check(self.L.gnna_aggregate_host(self.h, C.c_int(dt), _ptr(row_ptr), _ptr(col), C.c_uint32(n),

@@ -163,38 +163,6 @@ __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32
     stv<T, VEC>(y, val);
 }
 
-// Sequential gather over [b, e) into acc (CSR order; UNR loads in flight
-// per lane, added in edge order).
-template <class T, int VEC, int KMAX>
-__device__ __forceinline__ void gather(const AggArgs& a, uint64_t b, uint64_t e, const uint32_t (&off)[KMAX],
-                                       const bool (&ok)[KMAX], Vec<T, VEC> (&acc)[KMAX]) {
-    constexpr int UNR = 8 / KMAX;
-    const T* __restrict__ x = static_cast<const T*>(a.x);
-    const uint32_t* __restrict__ col = a.col;
-    uint64_t p = b;
-    for (; p + UNR <= e; p += UNR) {
-        uint32_t idx[UNR];
-#pragma unroll
-        for (int j = 0; j < UNR; ++j) idx[j] = __ldg(col + p + j);
-        Vec<T, VEC> val[UNR][KMAX];
-#pragma unroll
-        for (int j = 0; j < UNR; ++j)
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                if (ok[k]) val[j][k] = ldv<T, VEC>(x + (size_t)idx[j] * a.dim + off[k]);
-#pragma unroll
-        for (int j = 0; j < UNR; ++j)
-#pragma unroll
-            for (int k = 0; k < KMAX; ++k)
-                if (ok[k]) vadd(acc[k], val[j][k]);
-    }
-    for (; p < e; ++p) {
-        const uint32_t idx = __ldg(col + p);
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-            if (ok[k]) vadd(acc[k], ldv<T, VEC>(x + (size_t)idx * a.dim + off[k]));
-    }
-}
 
 // Occupancy vs. loads-in-flight, measured on B200 (profiles/README.md, r01
 // A/B): register-capped occupancy beats deep unrolling.  Wide teams (d >= 32
@@ -217,8 +185,8 @@ struct K3Tune {
     static constexpr int unr = KMAX == 1 ? unr1 : (KMAX == 2 ? (unr1 + 1) / 2 : (unr1 + 3) / 4);
 };
 
-// Team-cooperative gather over [b, e) into acc, same per-lane summation
-// order as `gather` (CSR order from 0).  The warp walks its teams' neighbour
+// Team-cooperative gather over [b, e) into acc: every output dimension is a
+// sequential sum in CSR order from 0 (engine.cpp:237-240).  The warp walks its teams' neighbour
 // lists in batches of 32 CSR entries: one coalesced index load per batch
 // (each lane holds 32/TEAM indices), indices are broadcast inside the team
 // with width-TEAM shuffles, and UNR x KMAX 16-byte row vectors per lane are

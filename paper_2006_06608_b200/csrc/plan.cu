@@ -132,6 +132,14 @@ __global__ void k2_violation(const uint32_t* __restrict__ t, uint64_t G, const u
         if ((u == 0 || t[u] != t[u - 1]) && first[t[u]] != u) atomicMin(bad, (unsigned long long)u);
 }
 
+__global__ void k_count_nonzero_u8(const uint8_t* __restrict__ f, uint64_t G, unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < G; u += (uint64_t)gridDim.x * blockDim.x)
+        c += f[u] != 0;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
 __global__ void k_max_u32(const uint32_t* __restrict__ t, uint64_t G, unsigned* __restrict__ out) {
     unsigned m = 0;
     for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < G; u += (uint64_t)gridDim.x * blockDim.x)
@@ -295,6 +303,15 @@ gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
                                                                           nullptr, plan->uflags.get(), us.get(),
                                                                           row_begin);
                     gnna::launched(ctx, "k2_plan");
+                }
+                {  // Algorithm-1 runs = leaders at the params' block width
+                    DevBuf<unsigned long long> cnt(1, s);
+                    GNNA_CUDA(cudaMemsetAsync(cnt.get(), 0, 8, s));
+                    k_count_nonzero_u8<<<gnna::grid_for(G, 256, 4096), 256, 0, s>>>(plan->leader.get(), G, cnt.get());
+                    gnna::launched(ctx, "k_count_nonzero_u8");
+                    unsigned long long r = 0;
+                    gnna::to_host(ctx, &r, cnt.get(), 1);
+                    plan->runs = r;
                 }
                 DevBuf<uint32_t> flag(G, s);
                 k2_carry_flags<<<gnna::grid_for(G, 256), 256, 0, s>>>(plan->uflags.get(), G, flag.get());

@@ -212,3 +212,16 @@ def test_host_stream_matches_per_batch(ctx, orc):
     ctx.aggregate_host_stream(p, batches)
     for (_, _, _, _, _, out), want in zip(batches, wants):
         assert np.array_equal(out.numpy(), want)
+
+
+def test_plan_info_runs_and_units(ctx, orc):
+    """plan_info: units = partition_neighbors count, runs = Algorithm-1 leaders."""
+    rng = np.random.default_rng(8)
+    for t in range(10):
+        n = int(rng.integers(1, 2000))
+        rp, col, _ = random_graph(rng, n, int(rng.integers(0, 8 * n + 1)))
+        kw = dict(ngs=int(rng.integers(1, 40)), dw=32, tpb=32 * int(rng.integers(1, 33)), dim=16)
+        _, tg, _, _ = orc.partition_neighbors(rp, col, kw["ngs"])
+        _, _, lead, _ = orc.build_mem_plan(tg, P(**kw).tolist()) if len(tg) else (None, None, np.zeros(0), 0)
+        info = ctx.plan(*to_dev(rp, col), P(**kw), 2).info()
+        assert info["groups"] == len(tg) and info["runs"] == int(np.sum(lead)), (t, info)
