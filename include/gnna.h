@@ -181,6 +181,11 @@ GNNA_API gnna_status gnna_simulate_cache_ranges(gnna_ctx* ctx, const uint32_t* d
                                        uint64_t cache_capacity, uint64_t cache_line,
                                        uint32_t dim, uint64_t* hits, uint64_t* accesses);
 
+/* engine.hpp:78 features_close on device data (same element count, same
+ * dtype): *close = 1 iff no element has |a-b| > rel_tol * max(|a|,|b|). */
+GNNA_API gnna_status gnna_features_close(gnna_ctx* ctx, int dtype, const void* d_a, const void* d_b,
+                                uint64_t count, double rel_tol, int* close);
+
 /* engine.hpp:66 aggregate_oracle: y[v] = sum in CSR order (K4). */
 GNNA_API gnna_status gnna_aggregate_rows(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,
                                 const uint32_t* d_col, uint32_t n, uint32_t dim,

@@ -212,6 +212,15 @@ class Context:
                                                C.c_uint32(n), C.c_uint32(x.shape[1]), _ptr(x), _ptr(out)))
         return out
 
+    def features_close(self, a, b, rel_tol):
+        """engine.cpp:162 features_close on device tensors (shape check here, elements on the GPU)."""
+        if tuple(a.shape) != tuple(b.shape) or a.dtype != b.dtype:
+            return False
+        out = C.c_int()
+        self._check(self.L.gnna_features_close(self.h, C.c_int(_dtype_code(a)), _ptr(a), _ptr(b),
+                                               C.c_uint64(a.numel()), C.c_double(rel_tol), C.byref(out)))
+        return bool(out.value)
+
     def aggregate_host(self, row_ptr, col, x, p: Params, strategy=WARP_SHARED, dim_mode=DIM_CYCLIC,
                        out=None, line=128, cache=None, want_cost=True):
         """gnna_aggregate_host: host (numpy / pinned torch CPU) buffers in and out."""

@@ -79,6 +79,15 @@ public:
     Dev(const Dev&) = delete;
     Dev& operator=(const Dev&) = delete;
     Dev(Dev&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; }
+    Dev& operator=(Dev&& o) noexcept {
+        if (this != &o) {
+            if (p_ && t_ctx.h) gnna_device_free(t_ctx.h, p_);
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+        }
+        return *this;
+    }
     ~Dev() {
         if (p_ && t_ctx.h) gnna_device_free(t_ctx.h, p_);
     }
@@ -720,32 +729,104 @@ ReorderResult reorder_edges(const EdgeList& el) {
     return r;
 }
 
+namespace {
+// Device-resident CSR built from device edges (to_csr semantics).
+struct DevGraph {
+    uint32_t n = 0;
+    uint64_t nnz = 0;
+    Dev<std::uint64_t> rp;
+    Dev<std::uint32_t> col;
+    DevGraph(const std::uint32_t* d_edges, std::uint64_t e, std::uint32_t nodes, bool sym)
+        : n(nodes), rp(std::size_t(nodes) + 1) {
+        ok(gnna_to_csr(ctx(), n, d_edges, e, sym, rp.get(), nullptr, &nnz));
+        col = Dev<std::uint32_t>(nnz);
+        ok(gnna_to_csr(ctx(), n, d_edges, e, sym, rp.get(), col.get(), &nnz));
+    }
+};
+}  // namespace
+
+// pipeline.cpp:93-124 with every stage's data kept on the GPU (SURVEY
+// §8(f)-3): the edge list is uploaded once, the symmetrised CSR, the
+// community assignment, the mapping, the renumbered graph, the plan, the
+// output and the verifying K4 oracle all stay in device memory; only the
+// value-type results the API returns (stats, mapping, params, report,
+// output) come back, plus the seeded features going up.
 RunResult run_pipeline(const EdgeList& el, const RunConfig& config) {
     RunResult res;
-    res.stats = analyze(el);
+    const std::uint64_t e = el.edges.size();
+    if (e == 0) throw DomainError("no edges in the input");  // aes (analyze) on an empty list
+    Dev<std::uint32_t> d_edges(flat_edges(el));
+    // analyze (pipeline.cpp:69-79)
+    res.stats.num_nodes = el.num_nodes;
+    res.stats.num_edges = e;
+    ok(gnna_aes(ctx(), d_edges.get(), e, &res.stats.aes));
+    res.stats.sqrt_aes = std::sqrt(res.stats.aes);
+    res.stats.threshold = std::floor(std::sqrt(static_cast<double>(el.num_nodes)) / 100.0);
+    res.stats.reorder = res.stats.sqrt_aes > res.stats.threshold;
+    std::unique_ptr<DevGraph> g = std::make_unique<DevGraph>(d_edges.get(), e, el.num_nodes, true);
+    if (el.num_nodes == 0) throw DomainError("degree_stats: graph has no nodes");
+    ok(gnna_degree_stats(ctx(), g->rp.get(), g->n, &res.stats.degrees.avg_degree, &res.stats.degrees.max_degree,
+                         &res.stats.degrees.stddev_degree));
     res.reordered = config.force_reorder.value_or(res.stats.reorder);
-    EdgeList work = el;
-    if (res.reordered) {
-        res.reorder = reorder_edges(el);
-        work = apply_mapping(el, res.reorder->mapping);
+    if (res.reordered) {  // reorder_edges (pipeline.cpp:81-91) + apply_mapping(el) (:101-102)
+        const std::uint32_t n = el.num_nodes;
+        Dev<std::uint32_t> com(n), o2n(n), n2o(n), moved(e * 2);
+        ReorderResult r;
+        ok(gnna_detect_communities(ctx(), g->rp.get(), g->col.get(), n, com.get(), &r.num_communities));
+        ok(gnna_build_mapping(ctx(), com.get(), n, r.num_communities, o2n.get(), n2o.get()));
+        ok(gnna_modularity(ctx(), g->rp.get(), g->col.get(), n, com.get(), r.num_communities, &r.modularity));
+        r.aes_before = res.stats.aes;
+        ok(gnna_apply_mapping_edges(ctx(), d_edges.get(), e, n, o2n.get(), moved.get()));
+        ok(gnna_aes(ctx(), moved.get(), e, &r.aes_after));
+        r.mapping.old_to_new = o2n.host(n);
+        r.mapping.new_to_old = n2o.host(n);
+        res.reorder = std::move(r);
+        g = std::make_unique<DevGraph>(moved.get(), e, n, true);  // to_csr(work, true)
     }
-    const CsrGraph g = to_csr(work, true);
     if (config.params) {
         res.params = *config.params;
         res.params.validate();
-    } else {
-        res.params = auto_params(ModelInputs::from_graph(g, config.dim));
+    } else {  // auto_params(ModelInputs::from_graph(g, dim)) on the device CSR
+        if (config.dim == 0) throw DomainError("dim must be positive");
+        gnna_model_inputs mi{};
+        ok(gnna_model_inputs_from_graph(ctx(), g->rp.get(), g->n, config.dim, &mi));
+        gnna_params p{};
+        decider_ok(gnna_auto_params(&mi, &p), "auto_params");
+        res.params = from_c(p);
     }
-    const FeatureMatrix x = random_features(g.num_nodes, res.params.dim, config.seed);
+    const FeatureMatrix x = random_features(g->n, res.params.dim, config.seed);
+    const Dev<double> dx(x.values);
+    Dev<double> dy(x.values.size()), dref(x.values.size());
     EngineOptions opts;
     opts.workers = config.workers;
     opts.cache = config.cache;
-    auto [y, report] = aggregate_scheduled(g, x, res.params, config.strategy, config.dim_mode, opts);
-    // pipeline.cpp:119-120: verify against the dense reference (K4 on the GPU)
-    if (!features_close(y, aggregate_oracle(g, x), 1e-12))
-        throw InternalError("simulated aggregation deviates from the dense reference");
-    res.report = report;
-    res.output = std::move(y);
+    if (opts.cache) opts.cache->validate();
+    const gnna_params c = to_c(res.params);
+    const int strat = config.strategy == Strategy::NaiveAtomic ? GNNA_NAIVE_ATOMIC
+                      : config.strategy == Strategy::UnitSync  ? GNNA_UNIT_SYNC
+                                                               : GNNA_WARP_SHARED;
+    const int mode = config.dim_mode == DimMode::Sequential ? GNNA_DIM_SEQUENTIAL : GNNA_DIM_CYCLIC;
+    gnna_plan* plan = nullptr;
+    ok(gnna_plan_create(ctx(), g->rp.get(), g->col.get(), g->n, 0, g->n, &c, strat, &plan));
+    std::unique_ptr<gnna_plan, void (*)(gnna_plan*)> hold(plan, gnna_plan_destroy);
+    ok(gnna_aggregate(ctx(), plan, GNNA_F64, mode, dx.get(), dy.get()));
+    gnna_cost cost{};
+    ok(gnna_cost_report(ctx(), plan, mode, opts.transaction_line_bytes, opts.cache ? opts.cache->capacity : 0,
+                        opts.cache ? opts.cache->line_size : 0, &cost));
+    // pipeline.cpp:119-120: verify against the dense reference (K4 + features_close on the GPU)
+    ok(gnna_aggregate_rows(ctx(), GNNA_F64, g->rp.get(), g->col.get(), g->n, res.params.dim, dx.get(), dref.get()));
+    int close = 0;
+    ok(gnna_features_close(ctx(), GNNA_F64, dy.get(), dref.get(), x.values.size(), 1e-12, &close));
+    if (!close) throw InternalError("simulated aggregation deviates from the dense reference");
+    res.report.atomic_ops = cost.atomic_ops;
+    res.report.global_reads = cost.global_reads;
+    res.report.global_writes = cost.global_writes;
+    res.report.global_transactions = cost.global_transactions;
+    res.report.shared_bytes_per_block = cost.shared_bytes_per_block;
+    res.report.cache_hits = cost.cache_hits;
+    res.report.cache_accesses = cost.cache_accesses;
+    res.output = FeatureMatrix(g->n, res.params.dim);
+    dy.to(res.output.values.data(), res.output.values.size());
     return res;
 }
 

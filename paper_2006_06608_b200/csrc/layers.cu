@@ -81,6 +81,20 @@ __global__ void k5_gcn_weights(const uint64_t* __restrict__ row_ptr, const uint3
     }
 }
 
+// engine.cpp:162-172 features_close: count elements with
+// |a-b| > tol * max(|a|, |b|) (NaN compares false there, and here).
+template <class T>
+__global__ void k_close_violations(const T* __restrict__ a, const T* __restrict__ b, uint64_t count, double tol,
+                                   unsigned long long* __restrict__ bad) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = (double)a[i], y = (double)b[i];
+        if (fabs(x - y) > tol * fmax(fabs(x), fabs(y))) ++c;
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+
 template <class T>
 __global__ void k_relu_mask(const T* __restrict__ u, const T* __restrict__ b, const T* __restrict__ dy, uint64_t m,
                             uint32_t q, T* __restrict__ du) {
@@ -248,6 +262,32 @@ gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
         gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, d_norm, d_self);
+    });
+}
+
+gnna_status gnna_features_close(gnna_ctx* ctx, int dtype, const void* d_a, const void* d_b, uint64_t count,
+                                double rel_tol, int* close) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        esize(dtype);
+        if (!close) gnna::raise(GNNA_ERR_DOMAIN, "features_close: null output");
+        DevBuf<unsigned long long> bad(1, ctx->stream);
+        GNNA_CUDA(cudaMemsetAsync(bad.get(), 0, 8, ctx->stream));
+        if (count) {
+            const unsigned grid = gnna::grid_for(count, 256, (uint64_t)ctx->num_sms * 8);
+            if (dtype == GNNA_F32)
+                k_close_violations<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(d_a),
+                                                                         static_cast<const float*>(d_b), count,
+                                                                         rel_tol, bad.get());
+            else
+                k_close_violations<double><<<grid, 256, 0, ctx->stream>>>(static_cast<const double*>(d_a),
+                                                                          static_cast<const double*>(d_b), count,
+                                                                          rel_tol, bad.get());
+            gnna::launched(ctx, "k_close_violations");
+        }
+        unsigned long long h = 0;
+        gnna::to_host(ctx, &h, bad.get(), 1);
+        *close = h == 0 ? 1 : 0;
     });
 }
 

@@ -133,6 +133,22 @@ def test_gin_backward_vs_oracle_and_autograd(ctx, orc):
         assert gde == pytest.approx(float(E.grad), rel=1e-9, abs=1e-11)
 
 
+def test_features_close_matches_reference_rule(ctx):
+    """engine.cpp:162-172: |a-b| <= tol*max(|a|,|b|) elementwise; NaN compares false (counts as close)."""
+    rng = np.random.default_rng(4)
+    a = rng.random(10000) - 0.5
+    b = a * (1 + 1e-13)
+    assert ctx.features_close(to_dev(a), to_dev(b), 1e-12)
+    b2 = b.copy()
+    b2[1234] *= 1 + 1e-9
+    assert not ctx.features_close(to_dev(a), to_dev(b2), 1e-12)
+    z = np.zeros(5)
+    assert ctx.features_close(to_dev(z), to_dev(z), 0.0)
+    n1 = np.array([np.nan, 1.0])
+    assert ctx.features_close(to_dev(n1), to_dev(np.array([5.0, 1.0])), 1e-12)
+    assert not ctx.features_close(to_dev(np.zeros(3)), to_dev(np.zeros(4)), 1.0)
+
+
 def test_backward_nonsymmetric_uses_transpose(ctx, orc):
     rng = np.random.default_rng(5)
     n = 200
