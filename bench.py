@@ -351,7 +351,8 @@ def run_ours(args):
                        "plan": plan.info(), "graph_build_s": round(gen_s, 3), "plan_build_s": round(plan_s, 3),
                        "max_degree": int(np.diff(rp_host).max())},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "frac": achieved / peak, "frac_of_nominal_8TBps": achieved / 8000.0,
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src, "kernel": "k3_aggregate (+k3b_fixup)", "kernel_ms": t_agg,
                          "algorithmic_bytes_per_launch": balg_rank},
             "cpu_baseline": cpu,

@@ -11,15 +11,35 @@ from __future__ import annotations
 import numpy as np
 
 
-def row_ranges(row_ptr_host, parts: int):
+def row_ranges(row_ptr_host, parts: int, community_starts=None, tol=0.01):
     """Contiguous row ranges with ~equal nnz: rank p starts at the first row
-    whose CSR offset reaches nnz*p/parts (binary search on row_ptr)."""
+    whose CSR offset reaches nnz*p/parts (binary search on row_ptr).
+
+    community_starts (sorted first rows of the renumbered communities, i.e.
+    the exclusive scan of community sizes after build_mapping) snaps each cut
+    to the nearest community boundary whose edge offset lies within
+    tol*nnz of the balanced cut, so a community stays on one rank when that
+    costs at most 1% of balance."""
     rp = np.asarray(row_ptr_host)
     n = len(rp) - 1
     nnz = int(rp[-1])
+    starts = np.asarray(community_starts, dtype=np.int64) if community_starts is not None else None
     cuts = [0]
     for p in range(1, parts):
-        cuts.append(int(np.searchsorted(rp, nnz * p / parts, side="left")))
+        target = nnz * p / parts
+        c = int(np.searchsorted(rp, target, side="left"))
+        if starts is not None and len(starts):
+            k = int(np.searchsorted(starts, c))
+            best = None
+            for s in (starts[k - 1] if k > 0 else None, starts[k] if k < len(starts) else None):
+                if s is None or not (0 <= s <= n):
+                    continue
+                dev = abs(float(rp[s]) - target)
+                if dev <= tol * nnz and (best is None or dev < best[0]):
+                    best = (dev, int(s))
+            if best is not None:
+                c = best[1]
+        cuts.append(c)
     cuts.append(n)
     cuts = [min(max(c, 0), n) for c in cuts]
     for i in range(1, len(cuts)):

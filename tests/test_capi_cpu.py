@@ -164,6 +164,14 @@ def test_row_ranges_balance():
         assert all(rr[i][1] == rr[i + 1][0] for i in range(parts - 1))
         loads = [int(rp[b] - rp[a]) for a, b in rr]
         assert max(loads) <= rp[-1] / parts + deg.max() + 1
+    # community snapping: cuts move to a community start when within 1% of nnz
+    starts = np.array([0, 1200, 2480, 3700, 4990])
+    snapped = row_ranges(rp, 4, community_starts=starts, tol=0.05)
+    plain = row_ranges(rp, 4)
+    for (a, _), (a0, _) in zip(snapped[1:], plain[1:]):
+        if a != a0:
+            assert a in starts and abs(int(rp[a]) - int(rp[a0])) <= 0.05 * rp[-1] + deg.max()
+    assert snapped[0][0] == 0 and snapped[-1][1] == 5000
     empty = row_ranges(np.array([0, 0, 0], np.uint64), 4)  # no edges: ranges still tile the rows
     assert empty[0][0] == 0 and empty[-1][1] == 2 and all(empty[i][1] == empty[i + 1][0] for i in range(3))
 
