@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-nodes", type=int, default=0, help="CPU-baseline sample size (nodes)")
     ap.add_argument("--flush-l2", action="store_true", help="force an L2 flush between steps")
+    ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gin"],
+                    help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized), gin (sum + (1+eps)x)")
     ap.add_argument("--evaluator", default="b200", choices=["b200", "reference"],
                     help="parameter choice: B200 cost model (default) or the reference's decider rules")
     return ap.parse_args()
@@ -262,8 +264,20 @@ def run_ours(args):
     flush = args.flush_l2 or x_bytes < 4 * l2
     scratch = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev) if flush else None
 
+    # --agg: sum = aggregate_scheduled; gcn = normalized_aggregate (engine.cpp:338-369)
+    # fused into K3 (per-edge norm[col], self weight, row scale); gin = sum + (1+eps) x
+    gw = ctx.gcn_weights(rp, col, False) if args.agg == "gcn" else None
+
+    def agg():
+        if args.agg == "gcn":
+            plan.aggregate_ex(x, out=y, node_weight=gw[0], self_weight=gw[1], row_scale=gw[0])
+        elif args.agg == "gin":
+            plan.aggregate_ex(x, out=y, alpha=1.0 + 0.1)
+        else:
+            plan.aggregate(x, out=y)
+
     def step():
-        plan.aggregate(x, out=y)
+        agg()
         if world > 1:
             allgather_rows(y, ranges, rank)
 
@@ -285,7 +299,7 @@ def run_ours(args):
         for i in range(args.steps):
             a, b, c = ev[i]
             a.record(stream)
-            plan.aggregate(x, out=y)
+            agg()
             b.record(stream)
             if world > 1:
                 allgather_rows(y, ranges, rank)
@@ -308,11 +322,15 @@ def run_ours(args):
 
     value = nnz * cfg.dim / (t_step * 1e-3)
     balg_rank = synth.b_alg(r1 - r0, my_nnz, cfg.dim)
+    if args.agg == "gcn":  # + per-edge weights, row scale and self weight per row
+        balg_rank += 8 * (r1 - r0) + 4 * n  # norm (row scale + gathered node weight) and self weights
+    elif args.agg == "gin":  # + the self row x[v]
+        balg_rank += 4 * cfg.dim * (r1 - r0)
     peak, peak_src = peaks()
     achieved = balg_rank / (t_agg * 1e-3) / 1e9
 
     # correctness spot check of this run against the CPU oracle on sampled rows
-    check = spot_check(rp_host, col, x, y, ranges if world > 1 else [(r0, r1)], cfg.dim)
+    check = spot_check(rp_host, col, x, y, ranges if world > 1 else [(r0, r1)], cfg.dim, agg=args.agg)
 
     # ---------------- e2e through the host-buffer C-ABI entry (pinned buffers)
     e2e = None
@@ -347,6 +365,9 @@ def run_ours(args):
             "config": {"workload": cfg.name, "n": n, "nnz": nnz, "dim": cfg.dim,
                        "params": {"ngs": p.ngs, "dw": p.dw, "tpb": p.tpb, "tpw": p.tpw},
                        "strategy": "WarpShared", "dim_mode": "Cyclic", "parallelism": f"rows{world}",
+                       "aggregation": {"sum": "aggregate_scheduled (sum)",
+                                       "gcn": "GCN normalized_aggregate D^-1/2 A D^-1/2 x (fused)",
+                                       "gin": "GIN sum + (1+eps) x, eps 0.1 (fused)"}[args.agg],
                        "l2": "flushed between steps" if flush else f"inputs ({x_bytes / 1e9:.2f} GB x) > L2 ({l2 / 1e6:.0f} MB)",
                        "plan": plan.info(), "graph_build_s": round(gen_s, 3), "plan_build_s": round(plan_s, 3),
                        "max_degree": int(np.diff(rp_host).max())},
@@ -366,30 +387,34 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def spot_check(rp_host, col, x, y, ranges, dim, rows=2000):
-    """fp32 result vs an fp64 CSR-order sum on sampled rows (rel. 1e-5)."""
+def spot_check(rp_host, col, x, y, ranges, dim, rows=2000, agg="sum"):
+    """fp32 result vs an fp64 recompute on sampled rows (rel. 1e-5): CSR-order
+    sum; for gcn norm[v] * sum norm[u] x[u] (norm = 1/sqrt(max(deg,1))); for gin
+    sum + 1.1 x[v]."""
     rng = np.random.default_rng(0)
     col_h = None
     worst = 0.0
+    deg = np.diff(rp_host).astype(np.float64)
+    norm = 1.0 / np.sqrt(np.maximum(deg, 1.0))
     for a, b in ranges:
         if b <= a:
             continue
         pick = np.unique(np.concatenate([rng.integers(a, b, size=rows), [a, b - 1]]))
         if col_h is None:
             col_h = col.cpu().numpy().view(np.uint32)
-        x_rows = {}
         ys = y[torch_index(pick, y.device)].cpu().numpy().astype(np.float64)
         for k, v in enumerate(pick):
             nb = col_h[rp_host[v]:rp_host[v + 1]]
-            if len(nb) == 0:
-                want = np.zeros(dim)
+            xs = x[torch_index(nb, x.device)].cpu().numpy().astype(np.float64) if len(nb) else np.zeros((0, dim))
+            if agg == "gcn":
+                want = norm[v] * (norm[nb][:, None] * xs).sum(0)
             else:
-                xs = x[torch_index(nb, x.device)].cpu().numpy().astype(np.float64)
                 want = xs.sum(0)
+                if agg == "gin":
+                    want = want + 1.1 * x[int(v)].cpu().numpy().astype(np.float64)
             err = np.abs(ys[k] - want) / np.maximum(np.abs(want), 1e-30)
             err[np.abs(ys[k] - want) == 0] = 0
             worst = max(worst, float(err.max()) if err.size else 0.0)
-        del x_rows
     return {"rows_checked": rows * len(ranges), "max_rel_err": worst, "tol": 1e-5, "ok": worst <= 1e-5}
 
 
@@ -488,7 +513,7 @@ def run_train(args):
     eb.record()
     torch.cuda.synchronize()
     t_agg = ea.elapsed_time(eb)
-    balg = synth.b_alg(n, nnz, hid) + 4 * nnz  # + per-edge weights
+    balg = synth.b_alg(n, nnz, hid) + 8 * n  # + norm and self weights
     peak, peak_src = peaks()
     del t16
     print(json.dumps({

@@ -142,15 +142,15 @@ GNNA_API gnna_status gnna_aggregate(gnna_ctx* ctx, const gnna_plan* plan, int dt
                            const void* d_x, void* d_y);
 /* Options of gnna_aggregate_ex: the fused forms the layer entry points need
  * (engine.cpp:338-408).  For each output row v of the plan:
- *   y[v] = relu?( row_scale[v] * ( sum_e edge_weight[e] * x[col[e]]
+ *   y[v] = relu?( row_scale[v] * ( sum_{u in N(v)} node_weight[u] * x[u]
  *                                  + self_weight[v] * x[v] ) )  (masked)
- * edge_weight is indexed by CSR position (F32 only; NULL = all ones);
+ * node_weight is per source node (F32 only; NULL = all ones; GCN: norm);
  * self_weight NULL uses the constant alpha (0 = no self term); row_scale NULL
  * = 1; mask (same shape/dtype as y) zeroes y where mask <= 0 (ReLU backward).
  * dim 0 = the plan's params.dim; any other width reuses the plan's schedule. */
 typedef struct {
     uint32_t dim;
-    const float* edge_weight;
+    const float* node_weight;
     const float* self_weight;
     double alpha;
     const float* row_scale;
@@ -236,8 +236,9 @@ GNNA_API gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, con
                           uint32_t n, int add_self_loops, double* d_norm, uint8_t* d_self);
 /* fp32 operands of the fused normalized aggregation (gnna_aggregate_ex):
  * d_row_scale[v] = norm[v], d_self_weight[v] = norm[v] if v gets an implicit
- * self loop else 0, d_edge_weight[e] = norm[col[e]] (any may be NULL).  Then
- * y = row_scale * (A_w x + self_weight * x) = D^-1/2 (A [+I]) D^-1/2 x. */
+ * self loop else 0, d_edge_weight[e] = norm[col[e]] (any may be NULL).  With
+ * node_weight = row_scale (= norm), gnna_aggregate_ex computes
+ * y = row_scale * (A (norm x) + self_weight * x) = D^-1/2 (A [+I]) D^-1/2 x. */
 GNNA_API gnna_status gnna_gcn_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
                              uint32_t n, int add_self_loops, float* d_row_scale,
                              float* d_self_weight, float* d_edge_weight);

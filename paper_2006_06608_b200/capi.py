@@ -73,7 +73,7 @@ class ModelInputs(C.Structure):
 
 class AggOpts(C.Structure):
     """gnna_agg_opts (include/gnna.h)."""
-    _fields_ = [("dim", C.c_uint32), ("edge_weight", C.c_void_p), ("self_weight", C.c_void_p), ("alpha", C.c_double),
+    _fields_ = [("dim", C.c_uint32), ("node_weight", C.c_void_p), ("self_weight", C.c_void_p), ("alpha", C.c_double),
                 ("row_scale", C.c_void_p), ("relu", C.c_int), ("mask", C.c_void_p)]
 
 
@@ -492,12 +492,12 @@ class Plan:
                                                   C.c_int(dim_mode), _ptr(x), _ptr(out)))
         return out
 
-    def aggregate_ex(self, x, out=None, edge_weight=None, self_weight=None, alpha=0.0, row_scale=None, relu=False,
+    def aggregate_ex(self, x, out=None, node_weight=None, self_weight=None, alpha=0.0, row_scale=None, relu=False,
                      mask=None, dim_mode=DIM_CYCLIC):
-        """gnna_aggregate_ex: y = relu?(row_scale * (A_w x + self_weight * x)) [masked]; x may be any width."""
+        """gnna_aggregate_ex: y = relu?(row_scale * (A (node_weight x) + self_weight * x)) [masked]; any width."""
         if out is None:
             out = self.ctx.torch.empty_like(x)
-        o = AggOpts(int(x.shape[1]), _ptr(edge_weight), _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu),
+        o = AggOpts(int(x.shape[1]), _ptr(node_weight), _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu),
                     _ptr(mask))
         self.ctx._check(self.ctx.L.gnna_aggregate_ex(self.ctx.h, self.h, C.c_int(_dtype_code(x)), C.c_int(dim_mode),
                                                      _ptr(x), _ptr(out), C.byref(o)))

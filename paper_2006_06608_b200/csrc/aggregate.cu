@@ -113,7 +113,7 @@ struct AggArgs {
     double alpha;         // EPI_SELF:  y += alpha * x[v]  (or sw[v] * x[v] when sw != null)
     const float* sw;      // EPI_SELF per-node self weights (GCN: norm[v] if v gets an implicit loop, else 0)
     const void* mask;     // EPI_MASK: y[v][d] = mask[v][d] > 0 ? y[v][d] : 0 (ReLU backward)
-    const float* ew;      // per-edge weights in CSR order (fp32 path): acc += ew[e] * x[col[e]]
+    const float* nw;      // per-source-node weights (fp32 path): acc += nw[u] * x[u], u = col[e]
     // K4 exact modes
     const double* norm;
     const uint8_t* self;
@@ -192,8 +192,10 @@ struct K3Tune {
 // with width-TEAM shuffles, and UNR x KMAX 16-byte row vectors per lane are
 // in flight before the in-order adds.  Loop bounds are warp-uniform (max
 // over the warp's teams), loads/adds of finished teams are predicated off.
-// EW (fp32 path): per-edge weights ew[e] (CSR order) ride along with the
-// indices; acc += ew[e] * x[col[e]] (one FMA per element).
+// EW (fp32 path): per-SOURCE-node weights nw[u] (GCN: norm[u]) gathered
+// beside the row vectors, acc += nw[col[e]] * x[col[e]] (one FMA per
+// element).  The weight load depends only on the index, so it issues with the
+// row loads (no extra latency level) and keeps nothing live across a batch.
 template <class T, int VEC, int TEAM, int KMAX, bool EW = false>
 __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64_t e, uint32_t lane,
                                             const uint32_t (&off)[KMAX], const bool (&ok)[KMAX],
@@ -204,14 +206,14 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
     const uint32_t* __restrict__ col = a.col;
     const uint32_t len = (uint32_t)(e - b);
     const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
+    // (A/B, r01: gathering the batch's weights once per lane and shuffling
+    // them like the indices spills on wide teams: C5 25.5 vs 17.6 ms.)
     for (uint32_t base = 0; base < wlen; base += 32) {
         uint32_t idxr[R];
-        float wr[EW ? R : 1];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t j = base + lane + r * TEAM;
             idxr[r] = j < len ? __ldg(col + b + j) : 0u;
-            if constexpr (EW) wr[r] = j < len ? __ldg(a.ew + b + j) : 0.f;
         }
         const uint32_t cnt = len > base ? min(32u, len - base) : 0u;
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, cnt);
@@ -221,17 +223,16 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
             uint32_t idx[UNR];
             float wgt[EW ? UNR : 1];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                idx[u] = __shfl_sync(0xffffffffu, idxr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
-                if constexpr (EW) wgt[u] = __shfl_sync(0xffffffffu, wr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
-            }
+            for (int u = 0; u < UNR; ++u) idx[u] = __shfl_sync(0xffffffffu, idxr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
             Vec<T, VEC> val[UNR][KMAX];
 #pragma unroll
-            for (int u = 0; u < UNR; ++u)
+            for (int u = 0; u < UNR; ++u) {
+                if constexpr (EW) wgt[u] = (uint32_t)(q0 + u) < cnt ? __ldg(a.nw + idx[u]) : 0.f;
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k)
                     if (ok[k] && (uint32_t)(q0 + u) < cnt)
                         val[u][k] = ldv<T, VEC>(x + (size_t)idx[u] * a.dim + off[k]);
+            }
 #pragma unroll
             for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -433,7 +434,7 @@ void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, con
     const unsigned threads = (a.upc * TEAM + 31) / 32 * 32;  // whole warps (gather_team is warp-collective)
     if (grid) {
         constexpr bool kEW = std::is_same<T, float>::value;  // weighted gathers: fp32 path only
-        if (a.ew && kEW) {
+        if (a.nw && kEW) {
             if (kmax == 1)
                 k3_aggregate<T, VEC, TEAM, 1, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
             else if (kmax == 2)
@@ -504,8 +505,8 @@ void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_
     if (dtype != GNNA_F32 && dtype != GNNA_F64) raise(GNNA_ERR_DOMAIN, "unknown dtype");
     const uint32_t dim = (o && o->dim) ? o->dim : plan->params.dim;
     const int elem = dtype == GNNA_F32 ? 4 : 8;
-    if (o && o->edge_weight && dtype != GNNA_F32)
-        raise(GNNA_ERR_DOMAIN, "aggregate: edge weights are supported on the F32 path only");
+    if (o && o->node_weight && dtype != GNNA_F32)
+        raise(GNNA_ERR_DOMAIN, "aggregate: node weights are supported on the F32 path only");
     const uint32_t wpb = plan->wpb;
     const Shape s = choose_shape(elem, dim, plan->params.dw, pow2floor(256 / wpb), x, y);
     // carry slots are sized for the widest dim seen on this plan
@@ -536,8 +537,7 @@ void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_
         a.alpha = o->alpha;
         a.scale = o->row_scale;
         a.mask = o->mask;
-        // edge weights are indexed by absolute CSR position (same as col)
-        a.ew = o->edge_weight;
+        a.nw = o->node_weight;
     }
     if (plan->G == 0 && plan->nempty == 0) return;
     const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;

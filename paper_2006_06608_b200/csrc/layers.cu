@@ -189,30 +189,28 @@ struct TransientPlan {
     }
 };
 
-// Row scale / self weight / per-edge weights of D^-1/2 (A [+I]) D^-1/2 with
-// the norms of the forward CSR (fwd) laid out on the CSR being aggregated
-// (tgt: the forward CSR itself, or its transpose for the adjoint).
+// norm (row scale and per-source node weight) and self weights of
+// D^-1/2 (A [+I]) D^-1/2 from the forward CSR's degrees; node-indexed, so the
+// same arrays serve the forward CSR and its transpose (the adjoint).
 struct GcnWeights {
-    DevBuf<float> rs, sw, ew;
+    DevBuf<float> rs, sw;
     GcnWeights(gnna_ctx* ctx, const uint64_t* fwd_rp, const uint32_t* fwd_col, const uint64_t* tgt_rp,
                const uint32_t* tgt_col, uint32_t n, int add_self) {
-        uint64_t nnz = 0;
-        gnna::to_host(ctx, &nnz, tgt_rp + n, 1);
         rs = DevBuf<float>(n ? n : 1, ctx->stream);
         sw = DevBuf<float>(n ? n : 1, ctx->stream);
-        ew = DevBuf<float>(nnz ? nnz : 1, ctx->stream);
         if (!n) return;
         DevBuf<double> norm(n, ctx->stream);
         DevBuf<uint8_t> self(n, ctx->stream);
         gcn_norm(ctx, fwd_rp, fwd_col, n, add_self, norm.get(), self.get());
         k5_gcn_weights<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, ctx->stream>>>(
-            tgt_rp, tgt_col, n, norm.get(), self.get(), rs.get(), sw.get(), ew.get());
+            tgt_rp, tgt_col, n, norm.get(), self.get(), rs.get(), sw.get(), nullptr);
         gnna::launched(ctx, "k5_gcn_weights");
     }
+    // K3 gathers norm[u] per edge (node_weight) and scales the row by norm[v]
     gnna_agg_opts opts(uint32_t dim) const {
         gnna_agg_opts o{};
         o.dim = dim;
-        o.edge_weight = ew.get();
+        o.node_weight = rs.get();
         o.self_weight = sw.get();
         o.row_scale = rs.get();
         return o;

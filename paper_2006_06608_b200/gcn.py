@@ -47,7 +47,7 @@ class GCN2:
         self.lr = lr
 
     def _agg(self, x, relu=False, mask=None, out=None):
-        return self.plan.aggregate_ex(x, out=out, edge_weight=self.ew, self_weight=self.sw, row_scale=self.rs,
+        return self.plan.aggregate_ex(x, out=out, node_weight=self.rs, self_weight=self.sw, row_scale=self.rs,
                                       relu=relu, mask=mask)
 
     def forward(self, x):

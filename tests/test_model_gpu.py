@@ -30,7 +30,7 @@ def ref_agg(rp, col, x, ew=None, sw=None, alpha=0.0, rs=None, relu=False, mask=N
     bound = np.zeros_like(y)
     for v in range(n):
         nb = col[rp[v]:rp[v + 1]]
-        w = ew[rp[v]:rp[v + 1]] if ew is not None else np.ones(len(nb))
+        w = ew[nb].astype(np.float64) if ew is not None else np.ones(len(nb))  # per source node
         y[v] = (w[:, None] * x[nb]).sum(0)
         bound[v] = (np.abs(w)[:, None] * np.abs(x[nb])).sum(0)
         c = sw[v] if sw is not None else alpha
@@ -58,7 +58,7 @@ def test_aggregate_ex_options(ctx, orc):
         plan = ctx.plan(drp, dcol, p, 2)
         for dim in (16, 22, 64, 3):
             x = rng.random((n, dim)) - 0.3
-            ew = rng.random(len(col)).astype(np.float32)
+            ew = rng.random(n).astype(np.float32)  # node weights
             sw = (rng.random(n) * (rng.random(n) < 0.5)).astype(np.float32)
             rs = rng.random(n).astype(np.float32)
             mask = rng.random((n, dim)) - 0.5
@@ -68,7 +68,7 @@ def test_aggregate_ex_options(ctx, orc):
             for o in opts:
                 want, bound = ref_agg(rp, col, x.astype(np.float32).astype(np.float64), o.get("ew"), o.get("sw"),
                                       o.get("alpha", 0.0), o.get("rs"), o.get("relu", False), o.get("mask"))
-                got = plan.aggregate_ex(dx, edge_weight=to_dev(o["ew"]) if "ew" in o else None,
+                got = plan.aggregate_ex(dx, node_weight=to_dev(o["ew"]) if "ew" in o else None,
                                         self_weight=to_dev(o["sw"]) if "sw" in o else None,
                                         alpha=o.get("alpha", 0.0), row_scale=to_dev(o["rs"]) if "rs" in o else None,
                                         relu=o.get("relu", False),
