@@ -183,6 +183,11 @@ struct K3Tune {
     static constexpr int minb = TEAM >= 8 ? 4 : 3;
 #endif
     static constexpr int unr = KMAX == 1 ? unr1 : (KMAX == 2 ? (unr1 + 1) / 2 : (unr1 + 3) / 4);
+#ifdef GNNA_K3_BATCH
+    static constexpr int batch = TEAM >= 8 ? 32 : GNNA_K3_BATCH;
+#else
+    static constexpr int batch = 32;
+#endif
 };
 
 // Team-cooperative gather over [b, e) into acc: every output dimension is a
@@ -201,24 +206,25 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
                                             const uint32_t (&off)[KMAX], const bool (&ok)[KMAX],
                                             Vec<T, VEC> (&acc)[KMAX]) {
     constexpr int UNR = K3Tune<TEAM, KMAX>::unr;
-    constexpr int R = 32 / TEAM;  // indices held per lane per batch
+    constexpr int BATCH = K3Tune<TEAM, KMAX>::batch;  // CSR entries per index batch
+    constexpr int R = BATCH / TEAM;                    // indices held per lane per batch
     const T* __restrict__ x = static_cast<const T*>(a.x);
     const uint32_t* __restrict__ col = a.col;
     const uint32_t len = (uint32_t)(e - b);
     const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
     // (A/B, r01: gathering the batch's weights once per lane and shuffling
     // them like the indices spills on wide teams: C5 25.5 vs 17.6 ms.)
-    for (uint32_t base = 0; base < wlen; base += 32) {
+    for (uint32_t base = 0; base < wlen; base += BATCH) {
         uint32_t idxr[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t j = base + lane + r * TEAM;
             idxr[r] = j < len ? __ldg(col + b + j) : 0u;
         }
-        const uint32_t cnt = len > base ? min(32u, len - base) : 0u;
+        const uint32_t cnt = len > base ? min((uint32_t)BATCH, len - base) : 0u;
         const uint32_t wcnt = __reduce_max_sync(0xffffffffu, cnt);
 #pragma unroll
-        for (int q0 = 0; q0 < 32; q0 += UNR) {
+        for (int q0 = 0; q0 < BATCH; q0 += UNR) {
             if ((uint32_t)q0 >= wcnt) break;
             uint32_t idx[UNR];
             float wgt[EW ? UNR : 1];
