@@ -78,6 +78,43 @@ def test_aggregate_ex_options(ctx, orc):
                 assert (err <= 1e-5 * (bound + np.abs(want)) + 1e-30).all(), (t, dim, list(o), float(err.max()))
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_torch_autograd_layers(ctx, orc, dtype):
+    """GCNConv / GINConv (torch.autograd over the C-ABI layer entry points)
+    vs the same model written with dense torch ops, float64 autograd."""
+    from paper_2006_06608_b200.torch_ops import GCNConv, GINConv
+    rng = np.random.default_rng(12)
+    n = 400
+    rp, col = powerlaw_graph(orc, rng, n, 1500)
+    drp, dcol = to_dev(rp, col)
+    torch.manual_seed(0)
+    l1 = GCNConv(ctx, 24, 16, self_loops=True, dtype=dtype)
+    l2 = GINConv(ctx, 16, 8, eps=0.2, dtype=dtype)
+    with torch.no_grad():
+        l2.bias.uniform_(-0.2, 0.2)
+    x = torch.tensor(rng.random((n, 24)) - 0.5, dtype=dtype, device="cuda", requires_grad=True)
+    y = l2(drp, dcol, torch.relu(l1(drp, dcol, x)))
+    g = torch.tensor(rng.random((n, 8)) - 0.5, dtype=dtype, device="cuda")
+    y.backward(g)
+    # dense float64 twin
+    An = torch.tensor(dense_norm_adj(rp, col, True), dtype=torch.float64)
+    A = torch.zeros((n, n), dtype=torch.float64)
+    for v in range(n):
+        A[v, torch.from_numpy(col[rp[v]:rp[v + 1]].astype(np.int64))] = 1.0
+    X = x.detach().double().cpu().requires_grad_(True)
+    W1 = l1.weight.detach().double().cpu().requires_grad_(True)
+    W2 = l2.weight.detach().double().cpu().requires_grad_(True)
+    B2 = l2.bias.detach().double().cpu().requires_grad_(True)
+    H = torch.relu(An @ X @ W1)
+    Y = torch.relu((A @ H + 1.2 * H) @ W2 + B2)
+    Y.backward(g.double().cpu())
+    tol = dict(rtol=1e-9, atol=1e-11) if dtype == torch.float64 else dict(rtol=1e-3, atol=1e-4)
+    np.testing.assert_allclose(y.detach().double().cpu().numpy(), Y.detach().numpy(), **tol)
+    for got, ref in ((x.grad, X.grad), (l1.weight.grad, W1.grad), (l2.weight.grad, W2.grad), (l2.bias.grad, B2.grad)):
+        r = ref.numpy()
+        np.testing.assert_allclose(got.double().cpu().numpy(), r, rtol=tol["rtol"], atol=tol["atol"] * max(1, np.abs(r).max()))
+
+
 def dense_norm_adj(rp, col, self_loops):
     n = len(rp) - 1
     A = np.zeros((n, n))
