@@ -3,11 +3,11 @@
 //
 // Shapes on this path are skinny: m = nodes (10^5..10^7), k and n = feature
 // widths (<= a few hundred).  At C3 (410k x 96 · 96 x 16) the product moves
-// 158 MB for 1.3 GFLOP (8 flop/B): it is HBM-bound, so the kernel is a
-// streaming SIMT kernel (coalesced A tiles staged in shared memory, W resident
-// in shared memory, one output row per thread) rather than a tensor-core
-// tile.  tcgen05 kind::tf32 would also break the 1e-5 fp32 parity bar
-// (SURVEY §7 hard part 5) for no speed gain at 8 flop/B.
+// 184 MB for 1.3 GFLOP: HBM-bound, but past what fp32 SIMT FMAs sustain at
+// HBM speed.  The fp32 product therefore runs on tcgen05 (gemm_tc.cu, 3xTF32
+// split so the 1e-5 parity bar holds) for k <= 128; the SIMT kernels below
+// (k6_gemm_pipe / k6_gemm_rows / k6_gemm_f32) serve k > 128 and the
+// GNNA_GEMM_SIMT=1 A/B switch.
 //
 // GEMM_EXACT (fp64 API): per output element the reference's order — k
 // ascending, a == 0 skipped, a separately rounded product added to the
@@ -20,6 +20,11 @@
 #include <type_traits>
 
 #include "gnna_common.cuh"
+
+namespace gnna {
+bool gemm_tc_f32(gnna_ctx* ctx, const float* a, const float* w, const float* bias, const double* row_scale,
+                 float* out, uint32_t m, uint32_t k, uint32_t n, int epilogue);  // gemm_tc.cu
+}
 
 namespace {
 
@@ -630,6 +635,11 @@ void launch_gemm(gnna_ctx* ctx, const GemmArgs& g, bool exact) {
     if (g.m == 0 || g.n == 0) return;
     if constexpr (std::is_same<T, float>::value) {
         if (!exact) {
+            static const bool simt = std::getenv("GNNA_GEMM_SIMT") != nullptr;  // A/B switch
+            if (!simt && gnna::gemm_tc_f32(ctx, static_cast<const float*>(g.a), static_cast<const float*>(g.w),
+                                           static_cast<const float*>(g.bias), g.row_scale, static_cast<float*>(g.out),
+                                           g.m, g.k, g.n, g.epilogue))
+                return;
             const uint32_t nj = g.n <= 4 ? 4 : g.n <= 8 ? 8 : g.n <= 16 ? 16 : 32;
             dim3 grid((g.m + ROWS - 1) / ROWS, (g.n + nj - 1) / nj);
             const size_t wbytes = (size_t)g.k * nj * 4;

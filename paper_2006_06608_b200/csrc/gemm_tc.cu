@@ -1,0 +1,655 @@
+// K6-TC: the fp32 node update X·W (engine.cpp:315-331 matmul, the fast path
+// of gcn_layer / gin_layer) on the 5th-generation tensor cores.
+//
+// tcgen05.mma kind::tf32 with the 3xTF32 split: every fp32 operand x is
+// written to shared memory as hi = rna_tf32(x) and lo = rna_tf32(x - hi), and
+// the product is accumulated in TMEM (fp32) as A_hi·W_hi + A_hi·W_lo +
+// A_lo·W_hi.  The dropped lo·lo term and the tf32 rounding of lo are ~2^-22
+// relative per product, so results stay inside the fp32 parity bar (1e-5 of
+// sum|terms|, tests/test_layers_gpu.py) that a plain tf32 MMA would break.
+//
+// Shape of the work: m = nodes (10^5..10^7) by small k, n (<= 128): HBM-bound
+// (C3: 410k x 96 . 96 x 16 moves 184 MB for 1.3 GFLOP).  Two kernels:
+//
+// k6_gemm_tc_tma (k % 4 == 0, 16-byte aligned A; the common case), persistent,
+// one CTA per SM, warp-specialised:
+//   * warp 8 issues TMA (cp.async.bulk.tensor, box 32 fp32 x 128 rows per K
+//     slice, SWIZZLE_128B) into an S-deep ring of stages and the MMAs;
+//   * the TMA'd tile IS the canonical SW128 K-major operand and, read as
+//     tf32, IS A_hi (truncated) -- it feeds tcgen05.mma straight from smem
+//     against [W_hi ; W_lo] (N = 2*NP: both cross terms in one instruction);
+//   * two groups of 4 warps take alternate tiles: each thread (= TMEM lane =
+//     tile row) reads its row from the swizzled stage (conflict-free), writes
+//     A_lo = rna_tf32(x - trunc(x)) into TMEM with tcgen05.st, and the MMA
+//     warp runs A_lo x W_hi with A from TMEM; the group then tcgen05.ld's its
+//     accumulator, adds the hi/lo column halves, applies the fused epilogue
+//     and stores the 32-row run of each warp coalesced via shared memory.
+//   Hand-offs are mbarriers only (no CTA-wide barrier in the loop).
+//
+// k6_gemm_tc (any k <= 128, any alignment): each thread loads its row into
+// registers one tile ahead, splits hi/lo into the no-swizzle K-major layout
+// (chunk c of row r at c*2048 + r*16: LBO 2048 B, SBO 128 B) and one thread
+// issues 3 MMAs per K step.
+//
+// Padding of k to KP and n to NP is zero-filled on chip only; HBM traffic stays
+// at the algorithmic m*(k+n)*4 bytes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "gnna_common.cuh"
+
+namespace gnna {
+
+namespace {
+
+constexpr int TM = 128;  // rows per tile = MMA M = TMEM lanes
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_NONE, K-major canonical layout
+// ((8,m),2):((16B,SBO),LBO); version 1 (sm_100), base offset 0.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+// Instruction descriptor kind::tf32: D f32, A/B tf32, both K-major, M=128.
+template <int NP>
+__device__ __forceinline__ constexpr uint32_t idesc_tf32() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NP >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    const long long t0 = clock64();
+    while (true) {
+        uint32_t done;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > (1ll << 34)) __trap();  // ~10 s: never hang the device
+    }
+}
+
+// 16 consecutive TMEM columns of this warp's 32 lanes -> 16 registers.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcArgs {
+    const float* a;
+    const float* w;
+    const float* bias;       // epilogue 1
+    const double* row_scale;  // epilogue 2
+    float* out;
+    uint32_t m, k, n;
+    int epilogue;  // 0 none, 1 bias + relu, 2 row scale
+    uint32_t tiles;
+    int vec;  // A rows are float4-loadable (k % 4 == 0, 16-byte aligned)
+};
+
+template <int KP, int NP>
+__global__ void __launch_bounds__(TM) k6_gemm_tc(TcArgs g) {
+    static_assert(KP % 8 == 0 && KP <= 128, "KP");
+    static_assert(NP % 16 == 0 && NP >= 16 && NP <= 64, "NP");
+    constexpr int KC = KP / 4;                  // 16-byte chunks per row
+    constexpr uint32_t A_CH = TM * 16;          // bytes per A chunk column (128 rows)
+    constexpr uint32_t W_CH = NP * 16;          // bytes per W chunk column (NP rows)
+    constexpr uint32_t A_BYTES = KC * A_CH;
+    constexpr uint32_t W_BYTES = KC * W_CH;
+    constexpr uint32_t TCOLS = NP < 32 ? 32 : NP;  // TMEM allocation: power of two >= 32
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* s_ahi = smem;
+    unsigned char* s_alo = smem + A_BYTES;
+    unsigned char* s_whi = smem + 2 * A_BYTES;
+    unsigned char* s_wlo = smem + 2 * A_BYTES + W_BYTES;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_slot;
+
+    const uint32_t t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const uint32_t j0 = blockIdx.y * NP;
+    const uint32_t nj = g.n - j0 < (uint32_t)NP ? g.n - j0 : (uint32_t)NP;
+
+    // W^T block (NP x KP, K-major), split once per CTA
+    for (uint32_t e = t; e < (uint32_t)(NP * KP); e += TM) {
+        const uint32_t nn = e / KP, kk = e % KP;
+        const float x = (nn < nj && kk < g.k) ? __ldg(g.w + (uint64_t)kk * g.n + j0 + nn) : 0.f;
+        const float hi = rna_tf32(x), lo = rna_tf32(x - hi);
+        const uint32_t off = (kk / 4) * W_CH + nn * 16 + (kk % 4) * 4;
+        *reinterpret_cast<float*>(s_whi + off) = hi;
+        *reinterpret_cast<float*>(s_wlo + off) = lo;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                     "r"(TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_slot;
+    const uint32_t bar_a = smem_u32(&bar);
+
+    float4 v[KC];  // this thread's row of the tile being loaded
+    auto load = [&](uint32_t tile) {
+        const uint64_t row = (uint64_t)tile * TM + t;
+        if (g.vec) {
+            const float4* src = reinterpret_cast<const float4*>(g.a + row * g.k);
+#pragma unroll
+            for (int c = 0; c < KC; ++c)
+                v[c] = (row < g.m && (uint32_t)c * 4 < g.k) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+            const float* src = g.a + row * g.k;
+#pragma unroll
+            for (int c = 0; c < KC; ++c) {
+                float e[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t kk = (uint32_t)c * 4 + q;
+                    e[q] = (row < g.m && kk < g.k) ? __ldg(src + kk) : 0.f;
+                }
+                v[c] = make_float4(e[0], e[1], e[2], e[3]);
+            }
+        }
+    };
+
+    constexpr uint32_t IDESC = idesc_tf32<NP>();
+    uint32_t parity = 0;
+    uint32_t tile = blockIdx.x;
+    if (tile < g.tiles) load(tile);
+    for (; tile < g.tiles; tile += gridDim.x) {
+        // the previous tile's MMAs completed (mbarrier) before its epilogue: smem is free
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+            float4 hi, lo;
+            hi.x = rna_tf32(v[c].x), lo.x = rna_tf32(v[c].x - hi.x);
+            hi.y = rna_tf32(v[c].y), lo.y = rna_tf32(v[c].y - hi.y);
+            hi.z = rna_tf32(v[c].z), lo.z = rna_tf32(v[c].z - hi.z);
+            hi.w = rna_tf32(v[c].w), lo.w = rna_tf32(v[c].w - hi.w);
+            *reinterpret_cast<float4*>(s_ahi + c * A_CH + t * 16) = hi;
+            *reinterpret_cast<float4*>(s_alo + c * A_CH + t * 16) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> tensor core
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t ahi = smem_u32(s_ahi), alo = smem_u32(s_alo);
+            const uint32_t whi = smem_u32(s_whi), wlo = smem_u32(s_wlo);
+#pragma unroll
+            for (int s = 0; s < KP / 8; ++s) {
+                const uint64_t dahi = smem_desc(ahi + 2 * s * A_CH, A_CH, 128);
+                const uint64_t dalo = smem_desc(alo + 2 * s * A_CH, A_CH, 128);
+                const uint64_t dwhi = smem_desc(whi + 2 * s * W_CH, W_CH, 128);
+                const uint64_t dwlo = smem_desc(wlo + 2 * s * W_CH, W_CH, 128);
+                mma_tf32(tmem, dalo, dwhi, IDESC, s > 0 ? 1u : 0u);  // small terms first
+                mma_tf32(tmem, dahi, dwlo, IDESC, 1u);
+                mma_tf32(tmem, dahi, dwhi, IDESC, 1u);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar_a)
+                         : "memory");
+        }
+        const uint32_t next = tile + gridDim.x;
+        if (next < g.tiles) load(next);  // in flight during the MMAs and the epilogue
+        mbar_wait(bar_a, parity);
+        parity ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float acc[NP];
+#pragma unroll
+        for (int c = 0; c < NP; c += 16) tmem_ld16(tmem + ((warp * 32u) << 16) + (uint32_t)c, acc + c);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+
+        const uint64_t row = (uint64_t)tile * TM + warp * 32 + lane;
+        if (row < g.m) {
+            if (g.epilogue == 1) {
+#pragma unroll
+                for (int j = 0; j < NP; ++j) {
+                    const float x = acc[j] + ((uint32_t)j < nj ? __ldg(g.bias + j0 + j) : 0.f);
+                    acc[j] = x > 0.f ? x : 0.f;
+                }
+            } else if (g.epilogue == 2) {
+                const float sc = (float)g.row_scale[row];
+#pragma unroll
+                for (int j = 0; j < NP; ++j) acc[j] *= sc;
+            }
+            float* o = g.out + row * g.n + j0;
+            if (nj == (uint32_t)NP && g.n % 4 == 0 && ((uintptr_t)o % 16 == 0)) {
+#pragma unroll
+                for (int j = 0; j < NP; j += 4)
+                    *reinterpret_cast<float4*>(o + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < NP; ++j)
+                    if ((uint32_t)j < nj) o[j] = acc[j];
+            }
+        }
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed variant (k % 4 == 0, 16-byte aligned A): the A tile arrives by
+// cp.async.bulk.tensor (box 32 fp32 x 128 rows per K slice, SWIZZLE_128B),
+// which IS the canonical SW128 K-major operand layout, so the raw fp32 tile
+// is A_hi as the tensor core reads it (tf32 = the top 19 bits).  The only
+// register pass is lo = rna_tf32(x - trunc_tf32(x)) written elementwise at the
+// same offsets (linear, conflict-free).  An S-deep ring of stages keeps S
+// tiles of HBM reads in flight while the CTA converts, multiplies and writes.
+// Two MMAs per K step: A_hi x [W_hi ; W_lo] (N = 2*NP, TMEM columns
+// [0,NP) and [NP,2NP)) and A_lo x W_hi (N = NP, onto columns [0,NP)); the
+// epilogue adds the two column halves.
+// ---------------------------------------------------------------------------
+
+// UMMA descriptor, SWIZZLE_128B K-major: rows of 128 B, 8-row atoms at SBO =
+// 1024 B (LBO unused, 1), layout type 2.  Atoms must be 1024-byte aligned.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
+}
+
+template <int KP, int NP>
+struct TmaCfg {
+    static constexpr int SL = KP / 32;           // K slices (128-byte rows)
+    static constexpr uint32_t SLICE = TM * 128;  // one slice of a 128-row tile (16 KB)
+    static constexpr uint32_t STAGE = SL * SLICE;
+    static constexpr uint32_t WSL = 2 * NP * 128;  // one slice of [W_hi^T ; W_lo^T]
+    static constexpr uint32_t WB = SL * WSL;
+    static constexpr uint32_t BUDGET = 224 * 1024;
+    static constexpr uint32_t OSTRIDE = NP + 1;              // output staging row stride (floats)
+    static constexpr uint32_t OUTB = 8 * 32 * OSTRIDE * 4;   // per-warp 32-row output staging
+    static constexpr int S0 = (int)((BUDGET - WB - OUTB) / STAGE);
+    static constexpr int S = S0 > 4 ? 4 : S0;  // TMA stages in flight
+    static constexpr size_t SMEM = (size_t)S * STAGE + WB + OUTB + 1024;  // + alignment slack
+    // TMEM columns: two accumulators [hi | lo-correction] of 2*NP, then two
+    // A_lo tiles of KP (lane = row, one tf32 per column)
+    static constexpr uint32_t ACC = 2 * NP;
+    static constexpr uint32_t LO0 = 2 * ACC;
+    static constexpr uint32_t NEED = LO0 + 2 * KP;
+    static constexpr uint32_t TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+    static_assert(NEED <= 512, "TMEM");
+};
+
+__device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ float lo_part(float x) { return rna_tf32(x - trunc_tf32(x)); }
+
+// 16 registers -> 16 consecutive TMEM columns of this warp's 32 lanes.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+        "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+        "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])));
+}
+
+// A from TMEM (A_lo), B from shared memory.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// Warp roles: two groups of four warps (group b = warps 4b..4b+3, thread =
+// TMEM lane = tile row) take alternate tiles (b = tile index & 1): each
+// converts A_lo into its TMEM buffer and runs the epilogue of its tile, so
+// one group's epilogue overlaps the other's conversion.  Warp 8 issues the
+// TMA loads and the MMAs.  Hand-offs are mbarriers: full[s] (TMA ->
+// converters), lo_full[b] (128 arrivals of group b -> MMA warp), mma_bar[b]
+// (tcgen05.commit -> group b's epilogue and the stage refill).
+constexpr int TC_CONV = 2 * TM;
+constexpr int TC_THREADS = TC_CONV + 32;
+
+template <int KP, int NP>
+__global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_constant__ CUtensorMap tmap, TcArgs g) {
+    using C = TmaCfg<KP, NP>;
+    constexpr int S = C::S;
+    static_assert(KP % 32 == 0 && S >= 2, "config");
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t full[S];
+    __shared__ uint64_t lo_full[2];
+    __shared__ uint64_t mma_bar[2];
+    __shared__ uint32_t tmem_slot;
+    const uint32_t raw_a = smem_u32(smem_raw);
+    const uint32_t base = (raw_a + 1023u) & ~1023u;
+    unsigned char* base_p = smem_raw + (base - raw_a);
+    const uint32_t w_a = base + S * C::STAGE;
+    unsigned char* w_p = base_p + S * C::STAGE;
+    float* ostage = reinterpret_cast<float*>(w_p + C::WB);
+
+    const uint32_t t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const uint32_t j0 = blockIdx.y * NP;
+    const uint32_t nj = g.n - j0 < (uint32_t)NP ? g.n - j0 : (uint32_t)NP;
+    const uint32_t my_tiles = g.tiles > blockIdx.x ? (g.tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    auto issue = [&](uint32_t i) {  // one thread: TMA of this CTA's i-th tile into stage i % S
+        const uint32_t s = i % S, tile = blockIdx.x + i * gridDim.x;
+        const uint32_t bar = smem_u32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(C::STAGE) : "memory");
+#pragma unroll
+        for (int sl = 0; sl < C::SL; ++sl)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(base + s * C::STAGE + sl * C::SLICE),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(sl * 32), "r"(tile * TM), "r"(bar)
+                : "memory");
+    };
+
+    if (t == TC_CONV) {  // MMA warp, lane 0: barriers, then the first S loads (overlap the W staging below)
+        for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+        for (int b = 0; b < 2; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&lo_full[b])), "r"(TM));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mma_bar[b])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        for (uint32_t i = 0; i < (uint32_t)S && i < my_tiles; ++i) issue(i);
+    }
+    if (t < TC_CONV) {
+        // [W_hi^T ; W_lo^T]: 2*NP rows, K-major, 128-byte swizzle (chunk ^= row % 8);
+        // all loads first so their latencies overlap
+        constexpr int PER = NP * KP / TC_CONV;
+        float wv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const uint32_t e = t + q * TC_CONV, nn = e / KP, kk = e % KP;
+            wv[q] = (nn < nj && kk < g.k) ? __ldg(g.w + (uint64_t)kk * g.n + j0 + nn) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const uint32_t e = t + q * TC_CONV, nn = e / KP, kk = e % KP;
+            const float hi = rna_tf32(wv[q]), lo = rna_tf32(wv[q] - hi);
+            const uint32_t sl = kk / 32, c = (kk % 32) / 4, b = (kk % 4) * 4;
+            const uint32_t r0 = nn, r1 = NP + nn;
+            *reinterpret_cast<float*>(w_p + sl * C::WSL + (r0 / 8) * 1024 + (r0 % 8) * 128 + ((c ^ (r0 % 8)) * 16) +
+                                      b) = hi;
+            *reinterpret_cast<float*>(w_p + sl * C::WSL + (r1 / 8) * 1024 + (r1 % 8) * 128 + ((c ^ (r1 % 8)) * 16) +
+                                      b) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // W (generic stores) -> tensor core
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                     "r"(C::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 8) {
+        // MMA issuer + stage refills
+        constexpr uint32_t IDESC_2N = idesc_tf32<2 * NP>();
+        constexpr uint32_t IDESC_N = idesc_tf32<NP>();
+        for (uint32_t i = 0; i < my_tiles; ++i) {
+            const uint32_t s = i % S, b = i & 1u;
+            mbar_wait(smem_u32(&lo_full[b]), (i >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t a_hi = base + s * C::STAGE;
+                const uint32_t d = tmem + b * C::ACC, a_lo = tmem + C::LO0 + b * KP;
+#pragma unroll
+                for (int sl = 0; sl < C::SL; ++sl)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t ao = sl * C::SLICE + q * 32, bo = sl * C::WSL + q * 32;
+                        mma_tf32(d, smem_desc_sw128(a_hi + ao), smem_desc_sw128(w_a + bo), IDESC_2N,
+                                 (sl | q) ? 1u : 0u);
+                        mma_tf32_ts(d, a_lo + sl * 32 + q * 8, smem_desc_sw128(w_a + bo), IDESC_N, 1u);
+                    }
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&mma_bar[b]))
+                    : "memory");
+            }
+            __syncwarp();
+            if (i >= 1) {
+                const uint32_t j = i - 1;
+                mbar_wait(smem_u32(&mma_bar[j & 1u]), (j >> 1) & 1u);  // MMA(j) has read stage j % S
+                if (lane == 0 && j + S < my_tiles) issue(j + S);
+                __syncwarp();
+            }
+        }
+    } else {
+        // converters / epilogue: thread r = TMEM lane r = tile row r
+        const uint32_t grp = warp / 4, wq = warp % 4;
+        const uint32_t lane_off = (wq * 32u) << 16;
+        const uint32_t r = wq * 32 + lane, r8 = r % 8;
+        const uint32_t row_off = (r / 8) * 1024 + r8 * 128;  // this thread's row inside a slice
+        for (uint32_t i = grp; i < my_tiles; i += 2) {
+            {
+                const uint32_t s = i % S, b = i & 1u;
+                mbar_wait(smem_u32(&full[s]), (i / S) & 1u);
+                // lo = rna_tf32(x - trunc_tf32(x)) of this thread's row, read from the
+                // swizzled tile (8 consecutive lanes hit 8 distinct bank groups)
+                const unsigned char* stg = base_p + s * C::STAGE + row_off;
+#pragma unroll
+                for (int sl = 0; sl < C::SL; ++sl) {
+                    float4 x[8];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        x[c] = *reinterpret_cast<const float4*>(stg + sl * C::SLICE + ((c ^ r8) * 16));
+                    float lo[32];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        lo[4 * c] = lo_part(x[c].x), lo[4 * c + 1] = lo_part(x[c].y);
+                        lo[4 * c + 2] = lo_part(x[c].z), lo[4 * c + 3] = lo_part(x[c].w);
+                    }
+                    const uint32_t col = tmem + lane_off + C::LO0 + b * KP + sl * 32;
+                    tmem_st16(col, lo);
+                    tmem_st16(col + 16, lo + 16);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lo_full[b])) : "memory");
+            }
+            const uint32_t j = i, bj = j & 1u;
+            mbar_wait(smem_u32(&mma_bar[bj]), (j >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float acc[2 * NP];
+#pragma unroll
+            for (int c = 0; c < 2 * NP; c += 16) tmem_ld16(tmem + lane_off + bj * C::ACC + (uint32_t)c, acc + c);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");  // ordered before the next lo_full arrival
+#pragma unroll
+            for (int q = 0; q < NP; ++q) acc[q] += acc[NP + q];
+
+            const uint64_t row0 = (uint64_t)(blockIdx.x + j * gridDim.x) * TM + wq * 32;
+            const uint64_t row = row0 + lane;
+            if (row < g.m) {
+                if (g.epilogue == 1) {
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const float x = acc[q] + ((uint32_t)q < nj ? __ldg(g.bias + j0 + q) : 0.f);
+                        acc[q] = x > 0.f ? x : 0.f;
+                    }
+                } else if (g.epilogue == 2) {
+                    const float sc = (float)g.row_scale[row];
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) acc[q] *= sc;
+                }
+            }
+            if (gridDim.y == 1) {
+                // the warp's 32 output rows are one contiguous run of 32*n floats:
+                // stage them (row stride NP+1: conflict-free) and store coalesced
+                float* st = ostage + warp * 32 * C::OSTRIDE;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) st[lane * C::OSTRIDE + q] = acc[q];
+                __syncwarp();
+                const uint32_t rows = row0 >= g.m ? 0u : (g.m - row0 < 32u ? (uint32_t)(g.m - row0) : 32u);
+                const uint32_t total = rows * g.n;
+                float* o = g.out + row0 * g.n;
+                uint32_t rr = lane / g.n, cc = lane % g.n;
+                const uint32_t dr = 32u / g.n, dc = 32u % g.n;
+                for (uint32_t e = lane; e < total; e += 32) {
+                    o[e] = st[rr * C::OSTRIDE + cc];
+                    rr += dr, cc += dc;
+                    if (cc >= g.n) cc -= g.n, ++rr;
+                }
+                __syncwarp();
+            } else if (row < g.m) {
+                float* o = g.out + row * g.n + j0;
+                if (nj == (uint32_t)NP && g.n % 4 == 0 && ((uintptr_t)o % 16 == 0)) {
+#pragma unroll
+                    for (int q = 0; q < NP; q += 4)
+                        *reinterpret_cast<float4*>(o + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NP; ++q)
+                        if ((uint32_t)q < nj) o[q] = acc[q];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+template <int KP, int NP>
+bool launch_tc_tma(gnna_ctx* ctx, const TcArgs& g) {
+    auto encode = tensor_map_encoder();
+    if (!encode) return false;
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {g.k, g.m};
+    const cuuint64_t strides[1] = {(cuuint64_t)g.k * 4};
+    const cuuint32_t box[2] = {32, (cuuint32_t)TM};
+    const cuuint32_t es[2] = {1, 1};
+    if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(g.a), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    using C = TmaCfg<KP, NP>;
+    auto kern = k6_gemm_tc_tma<KP, NP>;
+    static bool attr = [&] {
+        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+        return true;
+    }();
+    (void)attr;
+    const uint32_t cols = (g.n + NP - 1) / NP;
+    const uint32_t slots = (uint32_t)ctx->num_sms / cols;
+    dim3 grid(g.tiles < slots ? g.tiles : (slots ? slots : 1), cols);
+    kern<<<grid, TC_THREADS, C::SMEM, ctx->stream>>>(map, g);
+    launched(ctx, "k6_gemm_tc_tma");
+    return true;
+}
+
+template <int KP>
+bool launch_tma_n(gnna_ctx* ctx, const TcArgs& g) {
+    if (g.n <= 16) return launch_tc_tma<KP, 16>(ctx, g);
+    if (g.n <= 32 || KP > 96) return launch_tc_tma<KP, 32>(ctx, g);  // KP 128: 32-column blocks keep 2 stages
+    if constexpr (KP <= 96) return launch_tc_tma<KP, 64>(ctx, g);
+    return false;
+}
+
+template <int KP, int NP>
+void launch_tc(gnna_ctx* ctx, const TcArgs& g0) {
+    TcArgs g = g0;
+    constexpr size_t smem = (size_t)2 * (KP / 4) * TM * 16 + (size_t)2 * (KP / 4) * NP * 16;
+    auto kern = k6_gemm_tc<KP, NP>;
+    static int per_sm = [&] {
+        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int b = 0;
+        GNNA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, TM, smem));
+        return b < 1 ? 1 : b;
+    }();
+    const uint32_t cols = (g.n + NP - 1) / NP;
+    const uint32_t slots = (uint32_t)(ctx->num_sms * per_sm) / cols;
+    dim3 grid(g.tiles < slots ? g.tiles : (slots ? slots : 1), cols);
+    kern<<<grid, TM, smem, ctx->stream>>>(g);
+    GNNA_CUDA(cudaGetLastError());
+    launched(ctx, "k6_gemm_tc");
+}
+
+template <int KP>
+void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
+    if (g.n <= 16)
+        launch_tc<KP, 16>(ctx, g);
+    else if (g.n <= 32)
+        launch_tc<KP, 32>(ctx, g);
+    else
+        launch_tc<KP, 64>(ctx, g);
+}
+
+}  // namespace
+
+// out = a(m x k) · w(k x n) [+ bias, relu | * row_scale] on tcgen05.  Returns
+// false (nothing launched) for shapes this kernel does not take (k > 128).
+bool gemm_tc_f32(gnna_ctx* ctx, const float* a, const float* w, const float* bias, const double* row_scale,
+                 float* out, uint32_t m, uint32_t k, uint32_t n, int epilogue) {
+    if (k == 0 || k > 128 || m == 0 || n == 0) return false;
+    TcArgs g{a, w, bias, row_scale, out, m, k, n, epilogue, (m + TM - 1) / TM,
+             (k % 4 == 0 && ((uintptr_t)a % 16 == 0)) ? 1 : 0};
+    static const bool no_tma = std::getenv("GNNA_GEMM_TC_LD") != nullptr;  // A/B switch
+    if (g.vec && !no_tma) {
+        const bool ok = k <= 32 ? launch_tma_n<32>(ctx, g)
+                        : k <= 64 ? launch_tma_n<64>(ctx, g)
+                        : k <= 96 ? launch_tma_n<96>(ctx, g)
+                                  : launch_tma_n<128>(ctx, g);
+        if (ok) return true;
+    }
+    if (k <= 16)
+        launch_tc_n<16>(ctx, g);
+    else if (k <= 32)
+        launch_tc_n<32>(ctx, g);
+    else if (k <= 64)
+        launch_tc_n<64>(ctx, g);
+    else if (k <= 96)
+        launch_tc_n<96>(ctx, g);
+    else
+        launch_tc_n<128>(ctx, g);
+    return true;
+}
+
+}  // namespace gnna

@@ -15,17 +15,20 @@ from paper_2006_06608_b200.gcn import ctx_gemm_tn  # noqa: E402
 torch.backends.cuda.matmul.allow_tf32 = False
 
 
-def t(fn, reps=20):
+def t(fn, reps=20, batch=10):
+    """Median over `reps` of (CUDA-event time of `batch` back-to-back calls) / batch:
+    the device time per call with host launch overhead overlapped."""
     for _ in range(3):
         fn()
     ts = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        for _ in range(batch):
+            fn()
         b.record()
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) * 1000)
+        ts.append(a.elapsed_time(b) * 1000 / batch)
     return float(np.median(ts))
 
 

@@ -1,0 +1,76 @@
+"""GPU: the fp32 node update X·W on tcgen05 (gemm_tc.cu, 3xTF32 split, TMEM
+accumulator) vs an fp64 numpy product.  Bar: |err| <= 1e-5 * (|A|·|W|)
+elementwise (the fp32 parity bar of SURVEY §7 hard part 5), on shapes that
+cover every template instance (k padded to 16/32/64/96/128, n to 16/32/64
+with column blocks beyond 64), ragged m tails, k % 4 != 0 and unaligned A
+(the scalar-load path), both fused epilogues, k > 128 (SIMT fallback) and
+operands spanning many binades (where a single tf32 pass would fail).
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import to_dev
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1, 1, 1), (127, 8, 16), (128, 16, 16), (129, 22, 16), (300, 96, 16), (410, 16, 22), (1000, 24, 16),
+          (257, 33, 70), (2000, 64, 64), (777, 128, 32), (513, 100, 130), (4096, 96, 16), (300, 160, 16),
+          (40000, 96, 16)]
+
+
+def check(got, a, w, post=None):
+    want = a @ w
+    bound = np.abs(a) @ np.abs(w)
+    if post is not None:
+        want, bound = post(want, bound)
+    err = np.abs(got.astype(np.float64) - want)
+    ratio = float((err / np.maximum(bound, 1e-300)).max()) if err.size else 0.0
+    assert (err <= 1e-5 * bound + 1e-30).all(), ratio
+    return ratio
+
+
+@pytest.mark.parametrize("m,k,n", SHAPES)
+def test_gemm_tc_shapes(ctx, m, k, n):
+    rng = np.random.default_rng(m * 7 + k * 3 + n)
+    a = ((rng.random((m, k)) - 0.3) * np.exp2(rng.integers(-8, 8, (m, k)))).astype(np.float32)
+    w = ((rng.random((k, n)) - 0.5) * np.exp2(rng.integers(-6, 6, (k, n)))).astype(np.float32)
+    da, dw = to_dev(a, w)
+    got = ctx.gemm(da, dw).cpu().numpy()
+    check(got, a.astype(np.float64), w.astype(np.float64))
+
+
+def test_gemm_tc_epilogues_and_unaligned(ctx):
+    rng = np.random.default_rng(5)
+    m, k, n = 3001, 96, 16
+    a = (rng.random((m, k + 1)) - 0.5).astype(np.float32)
+    w = (rng.random((k, n)) - 0.5).astype(np.float32)
+    b = (rng.random(n) - 0.5).astype(np.float32)
+    s = rng.random(m)
+    dfull, dw, db, ds = to_dev(a, w, b, s)
+    da = dfull[:, 1:]  # row stride k+1 -> non-contiguous: the API packs it
+    a64 = a[:, 1:].astype(np.float64)
+    w64 = w.astype(np.float64)
+    check(ctx.gemm(da.contiguous(), dw).cpu().numpy(), a64, w64)
+    # 4-byte aligned but not 16-byte aligned A (offset view of a flat buffer)
+    flat = torch.zeros(m * k + 1, dtype=torch.float32, device="cuda")
+    flat[1:] = torch.from_numpy(np.ascontiguousarray(a[:, 1:])).cuda().reshape(-1)
+    view = flat[1:].view(m, k)
+    check(ctx.gemm(view, dw).cpu().numpy(), a64, w64)
+    b64 = b.astype(np.float64)
+    check(ctx.gemm(da.contiguous(), dw, db, 1).cpu().numpy(), a64, w64,
+          lambda y, bd: (np.maximum(0.0, y + b64), bd + np.abs(b64)))
+    check(ctx.gemm(da.contiguous(), dw, None, 2, ds).cpu().numpy(), a64, w64,
+          lambda y, bd: (s[:, None] * y, s[:, None] * bd))
+
+
+def test_gemm_tc_is_the_kernel_launched(ctx):
+    """The fp32 product runs k6_gemm_tc (not a SIMT fallback) for k <= 128,
+    as the CUDA profiler sees it."""
+    a, w = to_dev(np.ones((256, 96), np.float32), np.ones((96, 16), np.float32))
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        y = ctx.gemm(a, w)
+        torch.cuda.synchronize()
+    assert torch.equal(y, torch.full((256, 16), 96.0, device="cuda"))
+    names = [e.name for e in prof.events()]
+    assert any("k6_gemm_tc" in nm for nm in names), names
