@@ -24,6 +24,8 @@
 namespace gnna {
 bool gemm_tc_f32(gnna_ctx* ctx, const float* a, const float* w, const float* bias, const double* row_scale,
                  float* out, uint32_t m, uint32_t k, uint32_t n, int epilogue);  // gemm_tc.cu
+bool gemm_tn_tc_f32(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uint32_t p, uint32_t q,
+                    float* out);  // gemm_tc.cu
 }
 
 namespace {
@@ -703,6 +705,7 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
         return;
     }
     if constexpr (std::is_same<T, float>::value) {
+        if (gnna::gemm_tn_tc_f32(ctx, a, b, m, p, q, out)) return;
         if (p <= 128 && q <= 32) {
             const uint32_t pp = (p + 31) / 32;
             const uint32_t qb = q <= 4 ? 4 : q <= 8 ? 8 : q <= 16 ? 16 : 32;

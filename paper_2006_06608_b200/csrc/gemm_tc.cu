@@ -38,6 +38,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gnna_common.cuh"
 
@@ -622,6 +623,279 @@ void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
         launch_tc<KP, 64>(ctx, g);
 }
 
+// ---------------------------------------------------------------------------
+// dW = A^T B on tcgen05 (the backward of the update GEMM, gcn/gin_layer_backward):
+// a reduction over all m rows.  A (m x p) and B (m x q) are row-major, so as
+// MMA operands (M = feature of A, N = feature of B, K = row) both are
+// MN-major.  For tf32 the MN-major smem layout is the 128-byte swizzle with
+// 32-byte atomicity (layout type 1): 32-feature slices of BK rows, 4-row
+// 512-byte K atoms; the TMA mode CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes
+// exactly that, so the raw TMA'd stage IS A_hi / B_hi.
+//   * stage (S-deep ring): A[PS slices] | B_hi[QS] | B_lo[QS], where B_lo =
+//     rna_tf32(x - trunc(x)) is written elementwise by the converter warps at
+//     the same swizzled offsets, one LBO after B_hi: [B_hi | B_lo] is ONE
+//     N = 64*QS operand;
+//   * A_lo goes to TMEM (K-major there: lane = feature, column = row),
+//     written by the converter thread that owns the feature lane;
+//   * per K step: A_hi x [B_hi | B_lo] (SS, columns [0,32QS) and
+//     [32QS,64QS)) + A_lo x B_hi (TS, onto [0,32QS)), accumulated in TMEM
+//     for the CTA's whole run of BK-row blocks (split-K); the epilogue adds
+//     the two column halves.
+// M = 128 reads 4 A slices from the stage base: the 4 - PS phantom slices
+// alias the following bytes (in bounds) and only feed discarded rows of D.
+// Per-CTA partials are summed in CTA order by k6_tn_reduce (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int TN_BK = 64;
+
+template <int PS, int QS>
+struct TnCfg {
+    static constexpr uint32_t SL = TN_BK * 128;  // one 32-feature slice of a block (8 KB)
+    static constexpr uint32_t AH = 0, BH = PS * SL, BL = BH + QS * SL;
+    static constexpr uint32_t STAGE = (PS + 2 * QS) * SL;
+    static constexpr uint32_t TAIL = (4 - PS) * SL;  // phantom A slices past the last stage
+    static constexpr int S0 = (int)((224u * 1024u - TAIL) / STAGE);
+    static constexpr int S = S0 > 8 ? 8 : S0;
+    static constexpr size_t SMEM = (size_t)S * STAGE + TAIL + 1024;
+    static constexpr uint32_t ND = 64 * QS;                  // accumulator columns [hi.hi | hi.lo]
+    static constexpr int LOB = 4;                           // A_lo ring depth (TMEM)
+    static constexpr uint32_t LO0 = ND < 32 ? 32 : ND;      // A_lo buffers: LOB x BK columns
+    static constexpr uint32_t NEED = LO0 + LOB * TN_BK;
+    static constexpr uint32_t TCOLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+    static_assert(NEED <= 512, "TMEM");
+};
+
+// tf32, D f32, M = 128; A and B major-ness as given (bit 15 A, bit 16 B; 1 = MN-major).
+template <int N, int AMN, int BMN>
+__device__ __forceinline__ constexpr uint32_t idesc_tf32_mj() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMN << 15) | ((uint32_t)BMN << 16) |
+           ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
+
+// MN-major tf32 operand descriptor: layout type 1 (SWIZZLE_128B_BASE32B),
+// LBO = stride between 32-element MN groups, SBO = 512 (next 4-row K atom;
+// one K=8 MMA spans two).
+__device__ __forceinline__ uint64_t smem_desc_mn128(uint32_t addr, uint32_t lbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)(512 >> 4) << 32) | (1ull << 46) | (1ull << 61);
+}
+
+struct TnArgs {
+    uint32_t m, p, q;
+    uint32_t nblk, bpc;  // BK-row blocks, blocks per CTA
+    float* part;         // [gridDim.x][p][q]
+};
+
+constexpr int TN_THREADS = TM + 32;
+
+template <int PS, int QS>
+__global__ void __launch_bounds__(TN_THREADS, 1) k6_gemm_tn_tc(const __grid_constant__ CUtensorMap amap,
+                                                               const __grid_constant__ CUtensorMap bmap, TnArgs g) {
+    using C = TnCfg<PS, QS>;
+    constexpr int S = C::S;
+    static_assert(S >= 2, "stages");
+    extern __shared__ unsigned char smem_raw[];
+    constexpr int LOB = C::LOB;
+    __shared__ uint64_t full[S], empty[S], ready[LOB], lofree[LOB];
+    __shared__ uint32_t tmem_slot;
+    const uint32_t raw_a = smem_u32(smem_raw);
+    const uint32_t base = (raw_a + 1023u) & ~1023u;
+    unsigned char* base_p = smem_raw + (base - raw_a);
+    const uint32_t t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const uint32_t b0 = blockIdx.x * g.bpc;
+    const uint32_t nb = b0 >= g.nblk ? 0u : (g.nblk - b0 < g.bpc ? g.nblk - b0 : g.bpc);
+    constexpr uint32_t tx = (PS + QS) * C::SL;
+
+    auto issue = [&](uint32_t i) {  // one thread: TMA of local block i into stage i % S
+        const uint32_t s = i % S, row = (b0 + i) * TN_BK;
+        const uint32_t bar = smem_u32(&full[s]), st = base + s * C::STAGE;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+#pragma unroll
+        for (int sl = 0; sl < PS; ++sl)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(st + C::AH + sl * C::SL),
+                "l"(reinterpret_cast<uint64_t>(&amap)), "r"(sl * 32), "r"(row), "r"(bar)
+                : "memory");
+#pragma unroll
+        for (int sl = 0; sl < QS; ++sl)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(st + C::BH + sl * C::SL),
+                "l"(reinterpret_cast<uint64_t>(&bmap)), "r"(sl * 32), "r"(row), "r"(bar)
+                : "memory");
+    };
+
+    if (t == TM) {
+        for (int s = 0; s < S; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+        }
+        for (int b = 0; b < LOB; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&ready[b])), "r"(TM));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&lofree[b])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+        for (uint32_t i = 0; i < (uint32_t)S && i < nb; ++i) issue(i);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                     "r"(C::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 4) {
+        constexpr uint32_t ID_SS = idesc_tf32_mj<64 * QS, 1, 1>();
+        constexpr uint32_t ID_TS = idesc_tf32_mj<32 * QS, 0, 1>();
+        for (uint32_t i = 0; i < nb; ++i) {
+            const uint32_t s = i % S, b = i % LOB;
+            mbar_wait(smem_u32(&ready[b]), (i / LOB) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t st = base + s * C::STAGE;
+                const uint32_t alo = tmem + C::LO0 + b * TN_BK;
+#pragma unroll
+                for (int k8 = 0; k8 < TN_BK / 8; ++k8) {
+                    const uint32_t ko = k8 * 1024;
+                    const uint64_t da = smem_desc_mn128(st + C::AH + ko, C::SL);
+                    const uint64_t dbh = smem_desc_mn128(st + C::BH + ko, C::SL);
+                    mma_tf32(tmem, da, dbh, ID_SS, (i | (uint32_t)k8) ? 1u : 0u);  // [B_hi | B_lo]
+                    mma_tf32_ts(tmem, alo + k8 * 8, dbh, ID_TS, 1u);
+                }
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&empty[s]))
+                    : "memory");
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&lofree[b]))
+                    : "memory");
+            }
+            __syncwarp();
+            if (i >= 1) {
+                const uint32_t j = i - 1;
+                mbar_wait(smem_u32(&empty[j % S]), (j / S) & 1u);
+                if (lane == 0 && j + S < nb) issue(j + S);
+                __syncwarp();
+            }
+        }
+    } else {
+        const uint32_t lane_off = (warp * 32u) << 16;
+        for (uint32_t i = 0; i < nb; ++i) {
+            const uint32_t s = i % S, b = i % LOB;
+            mbar_wait(smem_u32(&full[s]), (i / S) & 1u);
+            if (i >= LOB) mbar_wait(smem_u32(&lofree[b]), ((i - LOB) / LOB) & 1u);  // MMA(i-LOB) read buffer b
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const unsigned char* st = base_p + s * C::STAGE;
+            // A_lo of feature t (TMEM lane t), rows 0..BK-1 -> columns; warps past PS*32 own phantom lanes
+            if (warp < (uint32_t)PS) {
+                const unsigned char* sa = st + C::AH + warp * C::SL;
+                const uint32_t c32 = lane / 8, w4 = (lane % 8) * 4;
+#pragma unroll
+                for (int k0 = 0; k0 < TN_BK; k0 += 16) {
+                    float lo[16];
+#pragma unroll
+                    for (int kk = 0; kk < 16; ++kk) {
+                        const uint32_t k = k0 + kk;
+                        const float x = *reinterpret_cast<const float*>(sa + (k / 4) * 512 + (k % 4) * 128 +
+                                                                        ((c32 ^ (k % 4)) * 32) + w4);
+                        lo[kk] = lo_part(x);
+                    }
+                    tmem_st16(tmem + lane_off + C::LO0 + b * TN_BK + k0, lo);
+                }
+            }
+            // B_lo, elementwise at the same swizzled offsets
+#pragma unroll
+            for (uint32_t f = t; f < QS * (C::SL / 16); f += TM) {
+                const float4 x = reinterpret_cast<const float4*>(st + C::BH)[f];
+                reinterpret_cast<float4*>(const_cast<unsigned char*>(st) + C::BL)[f] =
+                    make_float4(lo_part(x.x), lo_part(x.y), lo_part(x.z), lo_part(x.w));
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ready[b])) : "memory");
+        }
+        // epilogue: TMEM lane t = feature t of A
+        float* out = g.part + (size_t)blockIdx.x * g.p * g.q;
+        if (nb == 0) {
+            if (t < g.p)
+                for (uint32_t j = 0; j < g.q; ++j) out[t * g.q + j] = 0.f;
+        } else {
+            const uint32_t last = nb - 1;
+            mbar_wait(smem_u32(&lofree[last % LOB]), (last / LOB) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float acc[64 * QS];
+#pragma unroll
+            for (int c = 0; c < 64 * QS; c += 16) tmem_ld16(tmem + lane_off + (uint32_t)c, acc + c);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (t < g.p) {
+#pragma unroll
+                for (int j = 0; j < 32 * QS; ++j)
+                    if ((uint32_t)j < g.q) out[t * g.q + j] = acc[j] + acc[32 * QS + j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+}
+
+// out[o] = sum over chunks c (in order) of part[c][o]: deterministic.
+__global__ void k6_tn_reduce(const float* __restrict__ part, uint32_t chunks, uint32_t total, float* __restrict__ out) {
+    const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= total) return;
+    float sum = 0.f;
+    for (uint32_t c = 0; c < chunks; ++c) sum += part[(size_t)c * total + o];
+    out[o] = sum;
+}
+
+bool make_map(CUtensorMap* map, const float* ptr, uint32_t cols, uint32_t rows, uint32_t box_rows,
+              CUtensorMapSwizzle swz) {
+    auto encode = tensor_map_encoder();
+    if (!encode) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+    const cuuint32_t box[2] = {32, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int PS, int QS>
+bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uint32_t p, uint32_t q, float* out) {
+    CUtensorMap amap, bmap;
+    if (!make_map(&amap, a, p, m, TN_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+        !make_map(&bmap, b, q, m, TN_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+        return false;
+    using C = TnCfg<PS, QS>;
+    auto kern = k6_gemm_tn_tc<PS, QS>;
+    static bool attr = [&] {
+        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+        return true;
+    }();
+    (void)attr;
+    const uint32_t nblk = (m + TN_BK - 1) / TN_BK;
+    uint32_t ctas = nblk < (uint32_t)ctx->num_sms ? nblk : (uint32_t)ctx->num_sms;
+    const uint32_t bpc = (nblk + ctas - 1) / ctas;
+    ctas = (nblk + bpc - 1) / bpc;
+    const uint32_t total = p * q;
+    DevBuf<float> part((size_t)ctas * total, ctx->stream);
+    TnArgs g{m, p, q, nblk, bpc, part.get()};
+    kern<<<ctas, TN_THREADS, C::SMEM, ctx->stream>>>(amap, bmap, g);
+    launched(ctx, "k6_gemm_tn_tc");
+    k6_tn_reduce<<<(total + 255) / 256, 256, 0, ctx->stream>>>(part.get(), ctas, total, out);
+    launched(ctx, "k6_tn_reduce");
+    return true;
+}
+
 }  // namespace
 
 // out = a(m x k) · w(k x n) [+ bias, relu | * row_scale] on tcgen05.  Returns
@@ -650,6 +924,27 @@ bool gemm_tc_f32(gnna_ctx* ctx, const float* a, const float* w, const float* bia
     else
         launch_tc_n<128>(ctx, g);
     return true;
+}
+
+// out(p x q) = a(m x p)^T b(m x q) on tcgen05.  Returns false (nothing
+// launched) unless p, q are multiples of 4 (TMA row pitch), p <= 128, q <= 64
+// and both operands are 16-byte aligned.
+bool gemm_tn_tc_f32(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uint32_t p, uint32_t q, float* out) {
+    static const bool off = std::getenv("GNNA_GEMM_SIMT") != nullptr;  // A/B switch
+    if (off || m == 0 || p == 0 || q == 0 || p > 128 || q > 64 || p % 4 || q % 4 || (uintptr_t)a % 16 ||
+        (uintptr_t)b % 16)
+        return false;
+    const uint32_t ps = (p + 31) / 32;
+    auto go = [&](auto qs) {
+        constexpr int QS = decltype(qs)::value;
+        switch (ps) {
+            case 1: return launch_tn_tc<1, QS>(ctx, a, b, m, p, q, out);
+            case 2: return launch_tn_tc<2, QS>(ctx, a, b, m, p, q, out);
+            case 3: return launch_tn_tc<3, QS>(ctx, a, b, m, p, q, out);
+            default: return launch_tn_tc<4, QS>(ctx, a, b, m, p, q, out);
+        }
+    };
+    return q <= 32 ? go(std::integral_constant<int, 1>{}) : go(std::integral_constant<int, 2>{});
 }
 
 }  // namespace gnna

@@ -15,4 +15,8 @@ for w in c5 c3; do
 done
 for w in c1 c2 c3 c4; do timeout 600 python bench.py --workload $w --steps 20 --warmup 5 --no-e2e 2>/dev/null | tail -1; done > gpurun_out/sweep_$R.jsonl
 timeout 600 python bench.py --workload c3train --steps 20 --warmup 5 2>/dev/null | tail -1 > gpurun_out/c3train_$R.json
+timeout 300 python scripts/gemm_ab.py > gpurun_out/gemm_ab_$R.jsonl 2>&1
+GNNA_GEMM_SIMT=1 timeout 300 python scripts/gemm_ab.py > gpurun_out/gemm_ab_simt_$R.jsonl 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k6_gemm_tc -s 2 -c 1 -o /tmp/gemm_tc_$R python scripts/gemm_one.py 410236 96 16 3 > /dev/null 2>&1; echo ncu_gemm $?
+ncu -i /tmp/gemm_tc_$R.ncu-rep --page raw --csv > gpurun_out/gemm_tc_${R}_raw.csv 2>/dev/null
 du -sh gpurun_out

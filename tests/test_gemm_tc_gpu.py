@@ -74,3 +74,25 @@ def test_gemm_tc_is_the_kernel_launched(ctx):
     assert torch.equal(y, torch.full((256, 16), 96.0, device="cuda"))
     names = [e.name for e in prof.events()]
     assert any("k6_gemm_tc" in nm for nm in names), names
+
+
+TN_SHAPES = [(1, 4, 4), (31, 16, 16), (33, 96, 16), (1000, 96, 16), (5000, 16, 24), (4097, 64, 64), (2000, 128, 32),
+             (777, 100, 60), (3000, 16, 22), (410236, 96, 16)]
+
+
+@pytest.mark.parametrize("m,p,q", TN_SHAPES)
+def test_gemm_tn_tc(ctx, m, p, q):
+    """dW = A^T B (the backward product): tcgen05 for p, q % 4 == 0, SIMT
+    otherwise; fp32 result within 1e-5 of sum|a||b| (+ sqrt(m) fp32
+    accumulation allowance over the rows of each CTA's run)."""
+    from paper_2006_06608_b200.gcn import ctx_gemm_tn
+    rng = np.random.default_rng(m + p * 7 + q)
+    a = (rng.random((m, p)) - 0.5).astype(np.float32)
+    b = ((rng.random((m, q)) - 0.5) * np.exp2(rng.integers(-4, 4, (m, q)))).astype(np.float32)
+    da, db = to_dev(a, b)
+    got = ctx_gemm_tn(ctx, da, db).cpu().numpy().astype(np.float64)
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    want = a64.T @ b64
+    bound = np.abs(a64).T @ np.abs(b64)
+    err = np.abs(got - want)
+    assert (err <= 1e-5 * bound + 1e-30).all(), float((err / bound).max())
