@@ -260,7 +260,46 @@ def extra_workloads(ctx, dev, reps=10):
                         "algorithmic_GBps": balg / t / 1e9, "frac_of_measured_hbm": balg / t / 1e9 / peak,
                         "frac_of_nominal_8TBps": balg / t / 1e9 / 8000.0, "l2": "flushed between calls"})
         del plan, x, y, rp, col
+    out += update_gemms(ctx, dev, scratch, peak, reps)
     return out
+
+
+def update_gemms(ctx, dev, scratch, peak, reps):
+    """The C3 update GEMMs on tcgen05 (gemm_tc.cu, 3xTF32): X·W1 (n x 96 ·
+    96 x 16, the forward node update) and dW1 = X^T G (the backward
+    reduction).  Kernel time per call (CUDA events, L2 flushed), algorithmic
+    bytes 4·n·(k + n_out) against the measured HBM peak."""
+    import torch
+    from paper_2006_06608_b200 import synth
+    from paper_2006_06608_b200.gcn import ctx_gemm_tn
+    cfg = synth.CONFIGS["c3"]
+    n, k, q = cfg.n, 96, 16
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    x = torch.rand((n, k), generator=g, device=dev) - 0.5
+    w = torch.rand((k, q), generator=g, device=dev) - 0.5
+    gr = torch.rand((n, q), generator=g, device=dev) - 0.5
+    res = []
+    for name, call in (("X·W (update, k6_gemm_tc_tma)", lambda: ctx.gemm(x, w)),
+                       ("X^T·G (dW, k6_gemm_tn_tc)", lambda: ctx_gemm_tn(ctx, x, gr))):
+        for _ in range(3):
+            call()
+        ts = []
+        for _ in range(reps):
+            scratch.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            call()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = float(np.median(ts)) * 1e-3
+        balg = 4 * n * (k + q) + 4 * k * q
+        res.append({"workload": cfg.name, "gemm": name, "shape": [n, k, q], "dtype": "f32 (3xTF32 on tcgen05)",
+                    "kernel_ms": t * 1e3, "algorithmic_GBps": balg / t / 1e9,
+                    "frac_of_measured_hbm": balg / t / 1e9 / peak, "l2": "flushed between calls",
+                    "timing": "one call between events (includes the host-side launch)"})
+    return res
 
 
 # ------------------------------------------------------------------ our arm
