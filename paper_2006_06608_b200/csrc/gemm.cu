@@ -571,6 +571,98 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_warp(const float* __restrict__
 // thread (ti, tj) owns C[4ti..4ti+3][4tj..4tj+3]; rows staged 32 at a time
 // (float4, 16-byte aligned row strides).  Requires p, q multiples of 4 and
 // (p/4)(q/4) <= 1024.
+// dW = A^T B for small p*q with any p, q (the widths the tcgen05 path cannot
+// TMA, e.g. the 22-class output).  A CTA streams its row range in BK-row
+// blocks: each block of A (BK*p floats) and B (BK*q floats) is one contiguous
+// run in HBM, copied with 4-byte cp.async (coalesced, no alignment needs)
+// into a double-buffered shared tile while the previous block is consumed.
+// Thread = one TI x TJ output tile x one row group (rows k = grp mod rg of
+// each block); groups are summed in order in shared memory, CTA partials in
+// CTA order by the reduce kernel: deterministic.
+constexpr int TS_BK = 128;
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+
+template <int TI, int TJ>
+__global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict__ a, const float* __restrict__ b,
+                                                        uint32_t m, uint32_t p, uint32_t q, uint32_t rows_per_cta,
+                                                        float* __restrict__ part) {
+    extern __shared__ __align__(16) float sm[];
+    float* sa = sm;                          // [2][TS_BK * p]
+    float* sb = sm + 2 * TS_BK * p;          // [2][TS_BK * q]
+    const uint32_t tq = (q + TJ - 1) / TJ, tiles = ((p + TI - 1) / TI) * tq;
+    const uint32_t rg = blockDim.x / tiles;  // row groups (>= 1: checked by the host)
+    const uint32_t t = threadIdx.x, grp = t / tiles, tile = t % tiles;
+    const bool active = grp < rg;
+    const uint32_t ti = (tile / tq) * TI, tj = (tile % tq) * TJ;
+    const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_cta;
+    const uint64_t r_end = r_begin + rows_per_cta < m ? r_begin + rows_per_cta : m;
+    const uint32_t nblk = r_end > r_begin ? (uint32_t)((r_end - r_begin + TS_BK - 1) / TS_BK) : 0u;
+    auto load = [&](uint32_t blk, uint32_t buf) {
+        const uint64_t r0 = r_begin + (uint64_t)blk * TS_BK;
+        const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)TS_BK ? r_end - r0 : (uint64_t)TS_BK);
+        const float* ga = a + r0 * p;
+        const float* gb = b + r0 * q;
+        float* da = sa + (size_t)buf * TS_BK * p;
+        float* db = sb + (size_t)buf * TS_BK * q;
+        for (uint32_t e = t; e < nr * p; e += blockDim.x) cp_async4(da + e, ga + e);
+        for (uint32_t e = t; e < nr * q; e += blockDim.x) cp_async4(db + e, gb + e);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float acc[TI][TJ];
+#pragma unroll
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) acc[i][j] = 0.f;
+    if (nblk) load(0, 0);
+    for (uint32_t blk = 0; blk < nblk; ++blk) {
+        const uint32_t buf = blk & 1u;
+        if (blk + 1 < nblk) {
+            load(blk + 1, buf ^ 1u);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const uint64_t r0 = r_begin + (uint64_t)blk * TS_BK;
+        const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)TS_BK ? r_end - r0 : (uint64_t)TS_BK);
+        if (active) {
+            const float* xa = sa + (size_t)buf * TS_BK * p;
+            const float* xb = sb + (size_t)buf * TS_BK * q;
+            for (uint32_t k = grp; k < nr; k += rg) {
+                float av[TI], bv[TJ];
+#pragma unroll
+                for (int i = 0; i < TI; ++i) av[i] = ti + i < p ? xa[k * p + ti + i] : 0.f;
+#pragma unroll
+                for (int j = 0; j < TJ; ++j) bv[j] = tj + j < q ? xb[k * q + tj + j] : 0.f;
+#pragma unroll
+                for (int i = 0; i < TI; ++i)
+#pragma unroll
+                    for (int j = 0; j < TJ; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            }
+        }
+        __syncthreads();  // the buffer is refilled by the next iteration's load
+    }
+    // row groups -> shared memory (the staging area is free) -> sum in group order
+    float* red = sm;  // [rg][p*q]
+    const uint32_t total = p * q;
+    if (active)
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+            for (int j = 0; j < TJ; ++j)
+                if (ti + i < p && tj + j < q) red[(size_t)grp * total + (ti + i) * q + tj + j] = acc[i][j];
+    __syncthreads();
+    for (uint32_t o = t; o < total; o += blockDim.x) {
+        float sum = 0.f;
+        for (uint32_t g2 = 0; g2 < rg; ++g2) sum += red[(size_t)g2 * total + o];
+        part[(size_t)blockIdx.x * total + o] = sum;
+    }
+}
+
 constexpr int TN4_ROWS = 32;
 
 __global__ void k6_gemm_tn4(const float* __restrict__ a, const float* __restrict__ b, uint32_t m, uint32_t p,
@@ -706,6 +798,26 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
     }
     if constexpr (std::is_same<T, float>::value) {
         if (gnna::gemm_tn_tc_f32(ctx, a, b, m, p, q, out)) return;
+        constexpr uint32_t TI = 2, TJ = 4;
+        const uint32_t tiles = ((p + TI - 1) / TI) * ((q + TJ - 1) / TJ);
+        const size_t sbytes = std::max<size_t>((size_t)2 * TS_BK * (p + q), (size_t)(256 / std::max(tiles, 1u)) * p * q) * 4;
+        static const bool no_small = std::getenv("GNNA_TN_WARP") != nullptr;  // A/B switch
+        if (!no_small && tiles <= 256 && sbytes <= 96 * 1024) {
+            uint32_t ctas = std::max<uint32_t>(1, std::min<uint32_t>(4 * ctx->num_sms, (m + TS_BK - 1) / TS_BK));
+            const uint32_t rpc = ((m + ctas - 1) / ctas + TS_BK - 1) / TS_BK * TS_BK;
+            ctas = (m + rpc - 1) / rpc;
+            const uint32_t total = p * q;
+            DevBuf<float> part((size_t)ctas * total, ctx->stream);
+            if (sbytes > 48 * 1024)
+                GNNA_CUDA(cudaFuncSetAttribute(k6_gemm_tn_small<TI, TJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)sbytes));
+            k6_gemm_tn_small<TI, TJ><<<ctas, 256, sbytes, ctx->stream>>>(a, b, m, p, q, rpc, part.get());
+            gnna::launched(ctx, "k6_gemm_tn_small");
+            k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
+                part.get(), ctas, total, out);
+            gnna::launched(ctx, "k6_reduce_chunks_warp");
+            return;
+        }
         if (p <= 128 && q <= 32) {
             const uint32_t pp = (p + 31) / 32;
             const uint32_t qb = q <= 4 ? 4 : q <= 8 ? 8 : q <= 16 ? 16 : 32;

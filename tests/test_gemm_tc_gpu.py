@@ -77,13 +77,14 @@ def test_gemm_tc_is_the_kernel_launched(ctx):
 
 
 TN_SHAPES = [(1, 4, 4), (31, 16, 16), (33, 96, 16), (1000, 96, 16), (5000, 16, 24), (4097, 64, 64), (2000, 128, 32),
-             (777, 100, 60), (3000, 16, 22), (410236, 96, 16)]
+             (777, 100, 60), (3000, 16, 22), (410236, 96, 16), (410236, 16, 22), (5000, 7, 13), (1, 3, 5),
+             (20000, 30, 22), (1000, 130, 6)]
 
 
 @pytest.mark.parametrize("m,p,q", TN_SHAPES)
 def test_gemm_tn_tc(ctx, m, p, q):
-    """dW = A^T B (the backward product): tcgen05 for p, q % 4 == 0, SIMT
-    otherwise; fp32 result within 1e-5 of sum|a||b| (+ sqrt(m) fp32
+    """dW = A^T B (the backward product): tcgen05 for p, q % 4 == 0, the
+    cp.async-staged SIMT kernel for small p*q otherwise (k6_gemm_tn_small); fp32 result within 1e-5 of sum|a||b| (+ sqrt(m) fp32
     accumulation allowance over the rows of each CTA's run)."""
     from paper_2006_06608_b200.gcn import ctx_gemm_tn
     rng = np.random.default_rng(m + p * 7 + q)
