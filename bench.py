@@ -5,7 +5,8 @@ fraction of the aggregation kernel.  A "step" is one scheduled aggregation
 (aggregate_scheduled, engine.cpp:200-311: K3 + the K3b carry combine) of a
 device-resident fp32 feature matrix over the workload graph; with N > 1 ranks
 each rank owns a contiguous nnz-balanced row range and the step
-ends with the all-gather of output rows (NCCL).  Default workload: C5 (10M
+includes the all-gather of output rows: fused into K3 through symmetric memory
+(NVLS multimem.st or P2P stores) when available, else NCCL broadcasts.  Default workload: C5 (10M
 nodes, ~200M nnz, dim 128), whose inputs (x = 5.1 GB) are far larger than L2.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c4|c3|c2|c1]
@@ -51,6 +52,10 @@ def parse():
     ap.add_argument("--flush-l2", action="store_true", help="force an L2 flush between steps")
     ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gin"],
                     help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized), gin (sum + (1+eps)x)")
+    ap.add_argument("--multimem", action="store_true",
+                    help="N > 1: fused gather through the NVLS multicast address (multimem.st) instead of P2P stores")
+    ap.add_argument("--nccl-gather", action="store_true",
+                    help="N > 1: keep the NCCL broadcast-per-owner all-gather instead of the fused K3 fan-out")
     ap.add_argument("--evaluator", default="b200", choices=["b200", "reference"],
                     help="parameter choice: B200 cost model (default) or the reference's decider rules")
     return ap.parse_args()
@@ -308,7 +313,7 @@ def run_ours(args):
     import torch.distributed as dist
     from paper_2006_06608_b200 import synth
     from paper_2006_06608_b200.capi import WARP_SHARED, Context
-    from paper_2006_06608_b200.shard import allgather_rows, row_ranges
+    from paper_2006_06608_b200.shard import FusedRowGather, allgather_rows, row_ranges
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -359,8 +364,22 @@ def run_ours(args):
     # fused into K3 (per-edge norm[col], self weight, row scale); gin = sum + (1+eps) x
     gw = ctx.gcn_weights(rp, col, False) if args.agg == "gcn" else None
 
+    # multi-GPU: the all-gather fused into K3 through symmetric memory (NVLS
+    # multicast or P2P stores), else one NCCL broadcast per owner
+    fused = None
+    if world > 1 and args.agg == "sum" and not args.nccl_gather:
+        fused = FusedRowGather.create(tuple(x.shape), x.dtype, dev, multicast=args.multimem)
+        if fused is not None and not fused.verify(plan, x, ranges, rank):
+            fused = None  # a replica disagreed with the NCCL path: keep NCCL
+        if fused is not None:
+            y = fused.y
+    gather_mode = "single GPU" if world == 1 else (f"fused into K3 ({fused.mode})" if fused else
+                                                     "NCCL broadcast per owner (allgather_rows)")
+
     def agg():
-        if args.agg == "gcn":
+        if fused is not None:
+            fused.aggregate(plan, x)
+        elif args.agg == "gcn":
             plan.aggregate_ex(x, out=y, node_weight=gw[0], self_weight=gw[1], row_scale=gw[0])
         elif args.agg == "gin":
             plan.aggregate_ex(x, out=y, alpha=1.0 + 0.1)
@@ -369,7 +388,7 @@ def run_ours(args):
 
     def step():
         agg()
-        if world > 1:
+        if world > 1 and fused is None:
             allgather_rows(y, ranges, rank)
 
     for _ in range(args.warmup):
@@ -392,7 +411,7 @@ def run_ours(args):
             a.record(stream)
             agg()
             b.record(stream)
-            if world > 1:
+            if world > 1 and fused is None:
                 allgather_rows(y, ranges, rank)
             c.record(stream)
             if flush:
@@ -462,6 +481,8 @@ def run_ours(args):
             "config": {"workload": cfg.name, "n": n, "nnz": nnz, "dim": cfg.dim,
                        "params": {"ngs": p.ngs, "dw": p.dw, "tpb": p.tpb, "tpw": p.tpw},
                        "strategy": "WarpShared", "dim_mode": "Cyclic", "parallelism": f"rows{world}",
+                       "allgather": gather_mode,
+                       "ms_aggregate_vs_gather": [round(t_agg, 4), round(t_step - t_agg, 4)],
                        "aggregation": {"sum": "aggregate_scheduled (sum)",
                                        "gcn": "GCN normalized_aggregate D^-1/2 A D^-1/2 x (fused)",
                                        "gin": "GIN sum + (1+eps) x, eps 0.1 (fused)"}[args.agg],

@@ -160,6 +160,24 @@ typedef struct {
 GNNA_API gnna_status gnna_aggregate_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
                               const void* d_x, void* d_y, const gnna_agg_opts* opts);
 
+/* Multi-GPU row sharding with the all-gather fused into the aggregation
+ * (SURVEY §8(e) "fused target"; replaces aggregate + the per-layer
+ * ncclBroadcast-per-owner all-gather of the reference's sharded use).  Same
+ * as gnna_aggregate_ex on this rank's row-slice plan, and every final row
+ * value is ALSO written at the same row offset into
+ *   - each peer_y[i] (i < n_peer <= GNNA_MAX_PEERS): device pointers of the
+ *     other ranks' replicas of y, P2P-mapped into this context (NVLink stores
+ *     overlapped with the gather), or
+ *   - mc_y, when non-NULL: the NVLS multicast address bound to every rank's
+ *     replica of y (multimem.st; the switch writes all copies, this rank's
+ *     included, and d_y is not written separately).
+ * The caller orders the peers' reads after every rank's kernel (a stream-
+ * ordered cross-rank barrier).  Rows outside the plan are never written. */
+#define GNNA_MAX_PEERS 7
+GNNA_API gnna_status gnna_aggregate_fanout(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
+                                           const void* d_x, void* d_y, const gnna_agg_opts* opts,
+                                           void* const* peer_y, uint32_t n_peer, void* mc_y);
+
 /* engine.hpp:30-53 + engine.cpp:242-289: the integer CostReport of
  * aggregate_scheduled for this plan (K8).  cache_line == 0 disables the LRU
  * replay (EngineOptions::cache = nullopt). */

@@ -503,6 +503,23 @@ class Plan:
                                                      _ptr(x), _ptr(out), C.byref(o)))
         return out
 
+    def aggregate_fanout(self, x, out, peers=(), mc=None, self_weight=None, alpha=0.0, row_scale=None, relu=False,
+                         mask=None, dim_mode=DIM_CYCLIC):
+        """gnna_aggregate_fanout: aggregate_ex on this plan's rows, every final
+        row also written into each peer replica (device pointers or tensors:
+        the other ranks' y, P2P-mapped) or, with `mc`, only through the NVLS
+        multicast address of the replicated y."""
+        peers = [p if isinstance(p, int) else p.data_ptr() for p in peers]
+        if len(peers) > 7:
+            raise ValueError("at most 7 peer replicas (GNNA_MAX_PEERS)")
+        arr = (C.c_void_p * max(1, len(peers)))(*peers)
+        o = AggOpts(int(x.shape[1]), None, _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu), _ptr(mask))
+        mcp = None if mc is None else (mc if isinstance(mc, int) else mc.data_ptr())
+        self.ctx._check(self.ctx.L.gnna_aggregate_fanout(self.ctx.h, self.h, C.c_int(_dtype_code(x)),
+                                                         C.c_int(dim_mode), _ptr(x), _ptr(out), C.byref(o), arr,
+                                                         C.c_uint32(len(peers)), C.c_void_p(mcp)))
+        return out
+
     def cost(self, dim_mode=DIM_CYCLIC, line=128, cache=None):
         c = Cost()
         cap, cl = cache if cache else (0, 0)

@@ -63,6 +63,25 @@ __device__ __forceinline__ void stv(T* p, const Vec<T, VEC>& v) {
     }
 }
 
+// One row vector to the NVLS multicast address of a replicated y: the
+// NVSwitch writes it into every rank's copy (multimem.st, sm_90+).
+template <class T, int VEC>
+__device__ __forceinline__ void stv_multimem(T* p, const Vec<T, VEC>& v) {
+    if constexpr (sizeof(T) == 4 && VEC == 4) {
+        asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.a[0]),
+                     "f"(v.a[1]), "f"(v.a[2]), "f"(v.a[3])
+                     : "memory");
+    } else if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+            asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p + i), "f"(v.a[i]) : "memory");
+    } else {
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+            asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p + i), "d"(v.a[i]) : "memory");
+    }
+}
+
 template <class T, int VEC>
 __device__ __forceinline__ void vzero(Vec<T, VEC>& v) {
 #pragma unroll
@@ -114,6 +133,12 @@ struct AggArgs {
     const float* sw;      // EPI_SELF per-node self weights (GCN: norm[v] if v gets an implicit loop, else 0)
     const void* mask;     // EPI_MASK: y[v][d] = mask[v][d] > 0 ? y[v][d] : 0 (ReLU backward)
     const float* nw;      // per-source-node weights (fp32 path): acc += nw[u] * x[u], u = col[e]
+    // fused all-gather: final row values also go to the peer
+    // replicas of y (P2P stores over NVLink), or, when mc is set, only to the
+    // NVLS multicast address of the replicated y (every rank's copy, self included)
+    void* peers[GNNA_MAX_PEERS];
+    uint32_t npeer;
+    void* mc;
     // K4 exact modes
     const double* norm;
     const uint8_t* self;
@@ -134,7 +159,7 @@ struct Lanes {
     }
 };
 
-template <class T, int VEC>
+template <class T, int VEC, bool FAN = false>
 __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32_t off, Vec<T, VEC> val) {
     T* y = static_cast<T*>(a.y) + (size_t)v * a.dim + off;
     if (a.epi) {
@@ -160,7 +185,17 @@ __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32
             for (int i = 0; i < VEC; ++i) val.a[i] = m.a[i] > T(0) ? val.a[i] : T(0);
         }
     }
-    stv<T, VEC>(y, val);
+    if constexpr (FAN) {  // separate instantiations: the register-capped default K3 is untouched
+        if (a.mc) {
+            stv_multimem<T, VEC>(static_cast<T*>(a.mc) + (size_t)v * a.dim + off, val);
+            return;
+        }
+        stv<T, VEC>(y, val);
+        for (uint32_t i = 0; i < a.npeer; ++i)
+            stv<T, VEC>(static_cast<T*>(a.peers[i]) + (size_t)v * a.dim + off, val);
+    } else {
+        stv<T, VEC>(y, val);
+    }
 }
 
 
@@ -256,7 +291,7 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
 }
 
 // ----------------------------------------------------------------- K3 ---
-template <class T, int VEC, int TEAM, int KMAX, bool EW>
+template <class T, int VEC, int TEAM, int KMAX, bool EW, bool FAN = false>
 __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(AggArgs a) {
     using VT = Vec<T, VEC>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -286,7 +321,7 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(Ag
         if (active && direct) {
 #pragma unroll
             for (int k = 0; k < KMAX; ++k)
-                if (L.ok[k]) store_final<T, VEC>(a, v, L.off[k], acc[k]);
+                if (L.ok[k]) store_final<T, VEC, FAN>(a, v, L.off[k], acc[k]);
         }
         if (need_smem) {
             if (staged) {
@@ -315,7 +350,7 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(Ag
                 } else {
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k)
-                        if (L.ok[k]) store_final<T, VEC>(a, v, L.off[k], r[k]);
+                        if (L.ok[k]) store_final<T, VEC, FAN>(a, v, L.off[k], r[k]);
                 }
             }
             __syncthreads();
@@ -325,7 +360,7 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(Ag
 
 // K3b: split nodes add their carried run sums in block order (from 0);
 // empty rows get the epilogue of a zero sum.
-template <class T, int VEC, int TEAM>
+template <class T, int VEC, int TEAM, bool FAN = false>
 __global__ void __launch_bounds__(256) k3b_fixup(AggArgs a, const uint32_t* __restrict__ nodes,
                                                  const uint32_t* __restrict__ first,
                                                  const uint32_t* __restrict__ count, uint64_t nsplit,
@@ -343,7 +378,7 @@ __global__ void __launch_bounds__(256) k3b_fixup(AggArgs a, const uint32_t* __re
             const uint32_t cnt = count[i];
             for (uint32_t j = 0; j < cnt; ++j) vadd(acc, ldv<T, VEC>(cy + (size_t)j * a.dim));
         }
-        store_final<T, VEC>(a, v, c * VEC, acc);
+        store_final<T, VEC, FAN>(a, v, c * VEC, acc);
     }
 }
 
@@ -438,9 +473,18 @@ template <class T, int VEC, int TEAM>
 void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, const gnna_plan* plan) {
     const size_t smem = (size_t)a.upc * kmax * TEAM * sizeof(Vec<T, VEC>);
     const unsigned threads = (a.upc * TEAM + 31) / 32 * 32;  // whole warps (gather_team is warp-collective)
+    const bool fan = a.npeer || a.mc;
     if (grid) {
         constexpr bool kEW = std::is_same<T, float>::value;  // weighted gathers: fp32 path only
-        if (a.nw && kEW) {
+        if (fan) {  // fused all-gather: fp32 and fp64, unweighted gathers
+            if (a.nw) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_fanout: node weights are not supported");
+            if (kmax == 1)
+                k3_aggregate<T, VEC, TEAM, 1, false, true><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            else if (kmax == 2)
+                k3_aggregate<T, VEC, TEAM, 2, false, true><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            else
+                k3_aggregate<T, VEC, TEAM, 4, false, true><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+        } else if (a.nw && kEW) {
             if (kmax == 1)
                 k3_aggregate<T, VEC, TEAM, 1, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
             else if (kmax == 2)
@@ -457,8 +501,13 @@ void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, con
     }
     const uint64_t nfix = plan->nsplit + plan->nempty;
     if (nfix) {
-        k3b_fixup<T, VEC, TEAM><<<(unsigned)((nfix + 256 / TEAM - 1) / (256 / TEAM)), 256, 0, ctx->stream>>>(
-            a, plan->fix_nodes.get(), plan->fix_first.get(), plan->fix_count.get(), plan->nsplit, nfix);
+        const unsigned fgrid = (unsigned)((nfix + 256 / TEAM - 1) / (256 / TEAM));
+        if (fan)
+            k3b_fixup<T, VEC, TEAM, true><<<fgrid, 256, 0, ctx->stream>>>(
+                a, plan->fix_nodes.get(), plan->fix_first.get(), plan->fix_count.get(), plan->nsplit, nfix);
+        else
+            k3b_fixup<T, VEC, TEAM><<<fgrid, 256, 0, ctx->stream>>>(a, plan->fix_nodes.get(), plan->fix_first.get(),
+                                                                   plan->fix_count.get(), plan->nsplit, nfix);
         gnna::launched(ctx, "k3b_fixup");
     }
 }
@@ -505,8 +554,8 @@ namespace gnna {
 
 // Scheduled aggregation over a plan (K3 + K3b) with the optional epilogue
 // and per-edge weights of gnna_agg_opts (o may be null).
-void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
-                       const gnna_agg_opts* o) {
+void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                        const gnna_agg_opts* o, void* const* peers, uint32_t npeer, void* mc) {
     if (!plan) raise(GNNA_ERR_DOMAIN, "null plan");
     if (dtype != GNNA_F32 && dtype != GNNA_F64) raise(GNNA_ERR_DOMAIN, "unknown dtype");
     const uint32_t dim = (o && o->dim) ? o->dim : plan->params.dim;
@@ -545,6 +594,13 @@ void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_
         a.mask = o->mask;
         a.nw = o->node_weight;
     }
+    if (npeer > GNNA_MAX_PEERS) raise(GNNA_ERR_DOMAIN, "aggregate: at most GNNA_MAX_PEERS peer replicas");
+    for (uint32_t i = 0; i < npeer; ++i) {
+        if (!peers[i]) raise(GNNA_ERR_DOMAIN, "aggregate: null peer replica");
+        a.peers[i] = peers[i];
+    }
+    a.npeer = npeer;
+    a.mc = mc;
     if (plan->G == 0 && plan->nempty == 0) return;
     const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;
     if (grid > 0x7fffffffull) raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
@@ -555,6 +611,11 @@ void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_
         if (s.vec == 2) launch_k3<double, 2>(ctx, a, s, grid, plan);
         else launch_k3<double, 1>(ctx, a, s, grid, plan);
     }
+}
+
+void aggregate_plan_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
+                       const gnna_agg_opts* o) {
+    aggregate_plan_fan(ctx, plan, dtype, dim_mode, x, y, o, nullptr, 0, nullptr);
 }
 
 void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
@@ -618,6 +679,16 @@ gnna_status gnna_aggregate_ex(gnna_ctx* ctx, const gnna_plan* plan, int dtype, i
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
         gnna::aggregate_plan_ex(ctx, plan, dtype, dim_mode, d_x, d_y, opts);
+    });
+}
+
+gnna_status gnna_aggregate_fanout(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* d_x,
+                                  void* d_y, const gnna_agg_opts* opts, void* const* peer_y, uint32_t n_peer,
+                                  void* mc_y) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (n_peer && !peer_y) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_fanout: null peer list");
+        gnna::aggregate_plan_fan(ctx, plan, dtype, dim_mode, d_x, d_y, opts, peer_y, n_peer, mc_y);
     });
 }
 

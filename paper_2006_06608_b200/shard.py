@@ -56,3 +56,85 @@ def allgather_rows(y, ranges, rank, group=None):
         if b > a:
             dist.broadcast(y[a:b], src=p, group=group)
     return y
+
+
+class FusedRowGather:
+    """The per-layer all-gather fused into the aggregation (SURVEY §8(e),
+    "fused target").  The output y lives in torch symmetric memory, mapped
+    into every rank.  Each rank's K3 writes the final values of its own rows
+    straight into every replica (gnna_aggregate_fanout):
+
+    * "multimem": with NVLS (NVSwitch multicast), one multimem.st per row
+      vector to the multicast address writes all replicas, this rank's
+      included;
+    * "p2p": otherwise, P2P stores over NVLink into each peer's buffer beside
+      the local store.
+
+    Either way the transfer overlaps the gather, and no separate collective
+    pass runs.  A stream-ordered symmetric-memory barrier then orders every
+    rank's reads after all ranks' kernels.  `create` returns None when
+    symmetric memory is unavailable (one rank, gloo/CPU, no P2P), and the
+    caller keeps the NCCL `allgather_rows` path.  P2P is the default; the
+    NVLS multicast store is opt-in (`multicast=True`)."""
+
+    def __init__(self, y, handle, peers, mc, mode):
+        self.y, self.handle, self.peers, self.mc, self.mode = y, handle, peers, mc, mode
+
+    @staticmethod
+    def peer_pointers(buffer_ptrs, rank, offset=0):
+        """Device pointers of the other ranks' replicas (each rank's buffer
+        base + the tensor's byte offset inside it), in rank order."""
+        return [int(p) + offset for r, p in enumerate(buffer_ptrs) if r != rank]
+
+    @classmethod
+    def create(cls, shape, dtype, device, group=None, multicast=False):
+        try:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            if not dist.is_initialized() or dist.get_world_size(group) < 2:
+                return None
+            if dist.get_world_size(group) - 1 > 7:  # GNNA_MAX_PEERS
+                return None
+            y = symm.empty(*shape, dtype=dtype, device=device)
+            h = symm.rendezvous(y, group if group is not None else dist.group.WORLD)
+            ptrs = list(h.buffer_ptrs)
+            offset = y.data_ptr() - int(ptrs[h.rank])
+            if offset < 0:
+                return None
+            peers = cls.peer_pointers(ptrs, h.rank, offset)
+            mc = None
+            if multicast:
+                has = h.has_multicast_support
+                has = has() if callable(has) else has
+                if has and int(h.multicast_ptr):
+                    mc = int(h.multicast_ptr) + offset
+            y.zero_()
+            h.barrier(channel=0)
+            return cls(y, h, peers, mc, "multimem" if mc else "p2p")
+        except Exception:
+            return None
+
+    def aggregate(self, plan, x, **opts):
+        """This rank's rows into every replica, then the cross-rank barrier."""
+        if self.mc:
+            plan.aggregate_fanout(x, self.y, mc=self.mc, **opts)
+        else:
+            plan.aggregate_fanout(x, self.y, peers=self.peers, **opts)
+        self.handle.barrier(channel=0)
+        return self.y
+
+    def verify(self, plan, x, ranges, rank):
+        """One fused step against the NCCL path on a separate buffer, on every
+        rank; True only if all ranks agree bit for bit (the caller falls back
+        to allgather_rows otherwise)."""
+        import torch
+        import torch.distributed as dist
+        ref = torch.zeros_like(self.y)
+        plan.aggregate(x, out=ref)
+        allgather_rows(ref, ranges, rank)
+        self.y.zero_()
+        self.handle.barrier(channel=0)
+        self.aggregate(plan, x)
+        ok = torch.tensor([1 if torch.equal(self.y, ref) else 0], device=self.y.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        return bool(ok.item())

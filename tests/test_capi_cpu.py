@@ -253,3 +253,15 @@ def test_b200_evaluator_choices():
     assert 10_000 < t5 < 25_000
     mi0 = ModelInputs.make(dim=0)
     assert L.gnna_b200_auto_params(C.byref(mi0), C.c_uint64(1), C.c_double(0.0), C.byref(Params()), None) == 1
+
+
+def test_fused_row_gather_host_logic():
+    """FusedRowGather (the symmetric-memory fan-out of SURVEY §8(e)): peer
+    pointer order, and the NCCL fallback when symmetric memory cannot be set
+    up (no process group / one rank / CPU)."""
+    import torch
+    from paper_2006_06608_b200.shard import FusedRowGather
+    assert FusedRowGather.peer_pointers([10, 20, 30, 40], 2) == [10, 20, 40]
+    assert FusedRowGather.peer_pointers([5], 0) == []
+    assert FusedRowGather.peer_pointers([100, 200], 1, offset=8) == [108]
+    assert FusedRowGather.create((4, 4), torch.float32, "cpu") is None

@@ -1,0 +1,70 @@
+"""GPU: the all-gather fused into the aggregation (gnna_aggregate_fanout,
+SURVEY §8(e) "fused target").  On one GPU the "peer replicas" are local
+buffers, which exercises the kernel side exactly: every final row value of
+the rank's row-slice plan lands in y and in each replica at the same offset,
+rows outside the slice are never written, epilogues apply to every copy, and
+the fan-out instantiations give the same bits as the plain K3.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_graph, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def powerlaw(orc, rng, n, e, a=0.9):
+    w = 1.0 / np.arange(1, n + 1) ** a
+    src = rng.choice(n, size=e, p=w / w.sum())
+    edges = np.stack([src, rng.integers(0, n, size=e)], 1).astype(np.uint32)
+    return orc.to_csr(n, edges, True)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_fanout_writes_slice_rows_to_every_replica(ctx, orc, dtype):
+    from paper_2006_06608_b200.capi import Params
+    rng = np.random.default_rng(31)
+    for trial in range(6):
+        n = int(rng.integers(50, 5000))
+        rp, col = powerlaw(orc, rng, n, 8 * n) if trial % 2 else random_graph(rng, n, 5 * n, orc=orc)[:2]
+        drp, dcol = to_dev(rp, col)
+        dim = int(rng.choice([4, 16, 22, 64, 128]))
+        r0 = int(rng.integers(0, n // 2))
+        r1 = int(rng.integers(r0, n + 1))
+        p = Params.make(ngs=int(rng.choice([4, 16, 64])), dw=32, tpb=int(rng.choice([128, 256, 512])), dim=dim)
+        plan = ctx.plan(drp, dcol, p, rows=(r0, r1))
+        x = torch.tensor(rng.random((n, dim)) - 0.4, dtype=dtype, device="cuda")
+        want = torch.full((n, dim), 7.0, dtype=dtype, device="cuda")
+        plan.aggregate(x, out=want)
+        sentinel = -3.25
+        y = torch.full((n, dim), sentinel, dtype=dtype, device="cuda")
+        peers = [torch.full((n, dim), sentinel, dtype=dtype, device="cuda") for _ in range(int(rng.integers(1, 8)))]
+        plan.aggregate_fanout(x, y, peers=peers)
+        torch.cuda.synchronize()
+        for buf in [y] + peers:
+            assert torch.equal(buf[r0:r1], want[r0:r1]), (trial, dim, r0, r1)  # same bits as the plain K3
+            assert bool((buf[:r0] == sentinel).all()) and bool((buf[r1:] == sentinel).all())
+
+
+def test_fanout_epilogues_and_limits(ctx, orc):
+    from paper_2006_06608_b200.capi import DomainError, Params
+    rng = np.random.default_rng(5)
+    n = 3000
+    rp, col = powerlaw(orc, rng, n, 10 * n)
+    drp, dcol = to_dev(rp, col)
+    p = Params.make(ngs=16, dw=32, tpb=256, dim=32)
+    plan = ctx.plan(drp, dcol, p, rows=(100, 2500))
+    x = torch.tensor(rng.random((n, 32)) - 0.5, dtype=torch.float32, device="cuda")
+    rs = torch.tensor(rng.random(n), dtype=torch.float32, device="cuda")
+    want = torch.zeros((n, 32), device="cuda")
+    plan.aggregate_ex(x, out=want, alpha=1.1, row_scale=rs, relu=True)
+    y = torch.zeros((n, 32), device="cuda")
+    peers = [torch.zeros((n, 32), device="cuda") for _ in range(3)]
+    plan.aggregate_fanout(x, y, peers=peers, alpha=1.1, row_scale=rs, relu=True)
+    for buf in [y] + peers:
+        assert torch.equal(buf, want)
+    with pytest.raises(ValueError):
+        plan.aggregate_fanout(x, y, peers=[torch.zeros_like(y) for _ in range(8)])
+    with pytest.raises(DomainError):
+        plan.aggregate_fanout(x, y, peers=[0])  # null replica
