@@ -237,7 +237,7 @@ def extra_workloads(ctx, dev, reps=10):
         y = torch.empty_like(x)
         p, _ = ctx.b200_params(rp, cfg.dim)
         plan = ctx.plan(rp, col, p, WARP_SHARED)
-        rs, sw, _ = ctx.gcn_weights(rp, col, False)
+        rs, sw, _ = ctx.gcn_weights(rp, col, False, edge_weights=False)
         for agg in aggs:
             def call():
                 if agg == "gcn":
@@ -362,7 +362,7 @@ def run_ours(args):
 
     # --agg: sum = aggregate_scheduled; gcn = normalized_aggregate (engine.cpp:338-369)
     # fused into K3 (per-edge norm[col], self weight, row scale); gin = sum + (1+eps) x
-    gw = ctx.gcn_weights(rp, col, False) if args.agg == "gcn" else None
+    gw = ctx.gcn_weights(rp, col, False, edge_weights=False) if args.agg == "gcn" else None
 
     # multi-GPU: the all-gather fused into K3 through symmetric memory (NVLS
     # multicast or P2P stores), else one NCCL broadcast per owner

@@ -321,15 +321,17 @@ class Context:
                                          _ptr(norm), _ptr(sl)))
         return norm[:n], sl[:n]
 
-    def gcn_weights(self, row_ptr, col, self_loops=False):
-        """fp32 (row_scale[n], self_weight[n], edge_weight[nnz]) of D^-1/2 (A [+I]) D^-1/2."""
+    def gcn_weights(self, row_ptr, col, self_loops=False, edge_weights=True):
+        """fp32 (row_scale[n], self_weight[n], edge_weight[nnz] or None) of
+        D^-1/2 (A [+I]) D^-1/2.  The fused K3 only needs the node arrays
+        (edge_weights=False skips the per-edge array)."""
         n = row_ptr.numel() - 1
         torch = self.torch
         rs, sw = self._empty(max(n, 1), torch.float32), self._empty(max(n, 1), torch.float32)
-        ew = self._empty(max(col.numel(), 1), torch.float32)
+        ew = self._empty(max(col.numel(), 1), torch.float32) if edge_weights else None
         self._check(self.L.gnna_gcn_weights(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n), C.c_int(int(self_loops)),
                                             _ptr(rs), _ptr(sw), _ptr(ew)))
-        return rs[:n], sw[:n], ew[: col.numel()]
+        return rs[:n], sw[:n], (ew[: col.numel()] if edge_weights else None)
 
     def normalized_aggregate(self, row_ptr, col, x, norm, selfl, out=None):
         n = row_ptr.numel() - 1

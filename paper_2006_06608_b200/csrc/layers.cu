@@ -81,6 +81,17 @@ __global__ void k5_gcn_weights(const uint64_t* __restrict__ row_ptr, const uint3
     }
 }
 
+// Row scale and self weight only (the fused K3 gathers norm[u] itself):
+// thread per node, coalesced.
+__global__ void k5_gcn_node_weights(uint32_t n, const double* __restrict__ norm, const uint8_t* __restrict__ self,
+                                    float* __restrict__ rs, float* __restrict__ sw) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const double nv = norm[v];
+        rs[v] = (float)nv;
+        sw[v] = self[v] ? (float)nv : 0.f;
+    }
+}
+
 // engine.cpp:162-172 features_close: count elements with
 // |a-b| > tol * max(|a|, |b|) (NaN compares false there, and here).
 template <class T>
@@ -194,17 +205,24 @@ struct TransientPlan {
 // same arrays serve the forward CSR and its transpose (the adjoint).
 struct GcnWeights {
     DevBuf<float> rs, sw;
-    GcnWeights(gnna_ctx* ctx, const uint64_t* fwd_rp, const uint32_t* fwd_col, const uint64_t* tgt_rp,
-               const uint32_t* tgt_col, uint32_t n, int add_self) {
+    GcnWeights(gnna_ctx* ctx, const uint64_t* fwd_rp, const uint32_t* fwd_col, uint32_t n, int add_self) {
         rs = DevBuf<float>(n ? n : 1, ctx->stream);
         sw = DevBuf<float>(n ? n : 1, ctx->stream);
         if (!n) return;
         DevBuf<double> norm(n, ctx->stream);
         DevBuf<uint8_t> self(n, ctx->stream);
         gcn_norm(ctx, fwd_rp, fwd_col, n, add_self, norm.get(), self.get());
-        k5_gcn_weights<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, ctx->stream>>>(
-            tgt_rp, tgt_col, n, norm.get(), self.get(), rs.get(), sw.get(), nullptr);
-        gnna::launched(ctx, "k5_gcn_weights");
+        k5_gcn_node_weights<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(n, norm.get(), self.get(), rs.get(),
+                                                                              sw.get());
+        gnna::launched(ctx, "k5_gcn_node_weights");
+    }
+    // from norm/self arrays the caller already holds
+    GcnWeights(gnna_ctx* ctx, const double* norm, const uint8_t* self, uint32_t n) {
+        rs = DevBuf<float>(n ? n : 1, ctx->stream);
+        sw = DevBuf<float>(n ? n : 1, ctx->stream);
+        if (!n) return;
+        k5_gcn_node_weights<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(n, norm, self, rs.get(), sw.get());
+        gnna::launched(ctx, "k5_gcn_node_weights");
     }
     // K3 gathers norm[u] per edge (node_weight) and scales the row by norm[v]
     gnna_agg_opts opts(uint32_t dim) const {
@@ -230,7 +248,7 @@ void fast_gcn_forward(gnna_ctx* ctx, const uint64_t* rp, const uint32_t* col, ui
                       uint32_t in_dim, const void* w, uint32_t out_dim, int add_self, void* y) {
     if (!n) return;
     TransientPlan plan(ctx, rp, col, n, std::min(in_dim, out_dim));
-    GcnWeights gw(ctx, rp, col, rp, col, n, add_self);
+    GcnWeights gw(ctx, rp, col, n, add_self);
     if (out_dim < in_dim) {
         DevBuf<float> t((size_t)n * out_dim, ctx->stream);
         gnna::gemm(ctx, GNNA_F32, x, n, in_dim, w, out_dim, nullptr, 0, nullptr, t.get());
@@ -297,6 +315,12 @@ gnna_status gnna_gcn_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
         DevBuf<double> norm(n, ctx->stream);
         DevBuf<uint8_t> self(n, ctx->stream);
         gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, norm.get(), self.get());
+        if (!d_edge_weight && d_row_scale && d_self_weight) {
+            k5_gcn_node_weights<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(n, norm.get(), self.get(),
+                                                                                  d_row_scale, d_self_weight);
+            gnna::launched(ctx, "k5_gcn_node_weights");
+            return;
+        }
         k5_gcn_weights<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, ctx->stream>>>(
             d_row_ptr, d_col, n, norm.get(), self.get(), d_row_scale, d_self_weight, d_edge_weight);
         gnna::launched(ctx, "k5_gcn_weights");
@@ -383,7 +407,8 @@ struct NormAgg {
         : ctx(c), dtype(dt), rp(r), col(cl), n(nn), norm(nrm), self(slf) {
         if (dt == GNNA_F32 && nn) {
             plan = std::make_unique<TransientPlan>(c, r, cl, nn, dim);
-            w = std::make_unique<GcnWeights>(c, fwd_rp, fwd_col, r, cl, nn, add_self);
+            w = (nrm && slf) ? std::make_unique<GcnWeights>(c, nrm, slf, nn)
+                             : std::make_unique<GcnWeights>(c, fwd_rp, fwd_col, nn, add_self);
         }
     }
     void operator()(const void* x, void* y, uint32_t dim) const {

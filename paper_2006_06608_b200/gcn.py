@@ -37,7 +37,7 @@ class GCN2:
         self.params = params
         # one schedule (K1 units + K2 Algorithm-1 plan) for every aggregation of the step
         self.plan = ctx.plan(row_ptr, col, params, WARP_SHARED)
-        self.rs, self.sw, self.ew = ctx.gcn_weights(row_ptr, col, self_loops)
+        self.rs, self.sw, _ = ctx.gcn_weights(row_ptr, col, self_loops, edge_weights=False)
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
         self.w1 = ((torch.rand((in_dim, hidden), generator=g, device=dev) * 2 - 1) / math.sqrt(in_dim)).contiguous()
