@@ -229,7 +229,7 @@ def extra_workloads(ctx, dev, reps=10):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     scratch = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
     out = []
-    for w, aggs in (("c3", ("sum", "gcn", "gin")), ("c4", ("sum",))):
+    for w, aggs in (("c3", ("sum", "gcn", "gcn_gather", "gin")), ("c4", ("sum",))):
         cfg = synth.CONFIGS[w]
         _, rp, col = synth.build_graph(cfg, lambda n, e: ctx.to_csr(n, e, True), dev)
         nnz = int(col.numel())
@@ -238,9 +238,12 @@ def extra_workloads(ctx, dev, reps=10):
         p, _ = ctx.b200_params(rp, cfg.dim)
         plan = ctx.plan(rp, col, p, WARP_SHARED)
         rs, sw, _ = ctx.gcn_weights(rp, col, False, edge_weights=False)
+        xs = x * rs[:, None]  # the GCN layer's K3 input: norm * (X W) out of the update GEMM's epilogue
         for agg in aggs:
             def call():
-                if agg == "gcn":
+                if agg == "gcn":  # layer form: y = norm * (A xs [+ self * xs]); no implicit self loops here
+                    plan.aggregate_ex(xs, out=y, row_scale=rs)
+                elif agg == "gcn_gather":  # standalone form on an arbitrary x: K3 gathers norm[u] per edge
                     plan.aggregate_ex(x, out=y, node_weight=rs, self_weight=sw, row_scale=rs)
                 elif agg == "gin":
                     plan.aggregate_ex(x, out=y, alpha=1.1)
@@ -259,8 +262,12 @@ def extra_workloads(ctx, dev, reps=10):
                 ts.append(a.elapsed_time(b))
             t = float(np.median(ts)) * 1e-3
             balg = synth.b_alg(cfg.n, nnz, cfg.dim)
-            balg += {"gcn": 12 * cfg.n, "gin": 4 * cfg.dim * cfg.n}.get(agg, 0)
-            out.append({"workload": cfg.name, "aggregation": agg, "n": cfg.n, "nnz": nnz, "dim": cfg.dim,
+            balg += {"gcn": 4 * cfg.n, "gcn_gather": 12 * cfg.n, "gin": 4 * cfg.dim * cfg.n}.get(agg, 0)
+            form = {"gcn": "D^-1/2 (A [+I]) D^-1/2 as in the GCN layer: source scale in the update GEMM's "
+                           "epilogue, K3 = plain sum + destination scale + self term",
+                    "gcn_gather": "D^-1/2 (A [+I]) D^-1/2 x on an arbitrary x: K3 gathers norm[u] per edge",
+                    "gin": "sum + (1+eps) x", "sum": "aggregate_scheduled"}[agg]
+            out.append({"workload": cfg.name, "aggregation": agg, "form": form, "n": cfg.n, "nnz": nnz, "dim": cfg.dim,
                         "params": p.tolist()[:3], "kernel_ms": t * 1e3, "edge_dim_per_s": nnz * cfg.dim / t,
                         "algorithmic_GBps": balg / t / 1e9, "frac_of_measured_hbm": balg / t / 1e9 / peak,
                         "frac_of_nominal_8TBps": balg / t / 1e9 / 8000.0, "l2": "flushed between calls"})

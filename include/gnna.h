@@ -260,6 +260,18 @@ GNNA_API gnna_status gnna_gcn_norm(gnna_ctx* ctx, const uint64_t* d_row_ptr, con
 GNNA_API gnna_status gnna_gcn_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
                              uint32_t n, int add_self_loops, float* d_row_scale,
                              float* d_self_weight, float* d_edge_weight);
+/* Operands of the FOLDED normalisation (the GCN layer's fast form): when the
+ * aggregation's input comes from the update GEMM, the source-side D^-1/2 rides
+ * in the GEMM's row-scale epilogue (gnna_gemm epilogue 2 with d_norm), so the
+ * aggregation is a plain sum:
+ *   y = row_scale * (A t' + self_ind * t'),  t' = norm * (X W)
+ * d_norm[v] (f64) = norm[v] (the GEMM epilogue's row scale); d_row_scale[v] =
+ * norm[v]; d_row_scale2[v] = norm[v]^2 (an aggregation whose output feeds the
+ * next aggregation directly: its epilogue pre-scales it); d_self_ind[v] = 1 if
+ * v gets an implicit self loop else 0.  Any output may be NULL. */
+GNNA_API gnna_status gnna_gcn_fold_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
+                                           uint32_t n, int add_self_loops, double* d_norm, float* d_row_scale,
+                                           float* d_row_scale2, float* d_self_ind);
 /* engine.cpp:338-369 normalized_aggregate, z = D^-1/2 (A [+I]) D^-1/2 x,
  * F64 bitwise as the reference.  transpose != 0 applies the adjoint
  * (out[u] += norm[v]norm[u] x[v]); it requires the transposed CSR
@@ -372,8 +384,10 @@ GNNA_API gnna_status gnna_search_params(const gnna_model_inputs* in, uint32_t it
  * L2/HBM figures.  Fills `in` device fields from the live device. */
 GNNA_API gnna_status gnna_b200_profile(gnna_ctx* ctx, gnna_model_inputs* in);
 /* B200 evaluator (north-star subsystem 3): picks ngs from a calibrated
- * cost model T(ngs) = max(B_alg/BW + G(ngs)*c_unit, min(ngs, max_degree)*c_edge)
- * with G = n + nnz/ngs; tpb = 512; dw = select_dw(dim).  hbm_gbs <= 0 uses
+ * cost model T(ngs) = max(B_alg/BW + G(ngs)*c_unit,
+ *                         c_ramp*B_alg/BW + min(ngs, max_degree)*c_edge)
+ * with G = n + nnz/ngs (c_unit 24 ps, c_edge 95 ns, c_ramp 0.46, fitted on
+ * measured K3 sweeps); tpb = 512; dw = select_dw(dim).  hbm_gbs <= 0 uses
  * 6553 (MEASURED_PEAKS.json).  *est_us (may be NULL) = the model's K3 time. */
 GNNA_API gnna_status gnna_b200_auto_params(const gnna_model_inputs* in, uint64_t max_degree, double hbm_gbs,
                                   gnna_params* out, double* est_us);

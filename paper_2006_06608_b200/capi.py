@@ -333,6 +333,19 @@ class Context:
                                             _ptr(rs), _ptr(sw), _ptr(ew)))
         return rs[:n], sw[:n], (ew[: col.numel()] if edge_weights else None)
 
+    def gcn_fold_weights(self, row_ptr, col, self_loops=False):
+        """gnna_gcn_fold_weights: (norm f64, row_scale = norm, row_scale2 =
+        norm^2, self indicator) for the folded normalisation, whose source-side
+        D^-1/2 rides in the producing GEMM's row-scale epilogue."""
+        n = row_ptr.numel() - 1
+        torch = self.torch
+        norm = self._empty(max(n, 1), torch.float64)
+        rs, rs2, ind = (self._empty(max(n, 1), torch.float32) for _ in range(3))
+        self._check(self.L.gnna_gcn_fold_weights(self.h, _ptr(row_ptr), _ptr(col), C.c_uint32(n),
+                                                 C.c_int(int(self_loops)), _ptr(norm), _ptr(rs), _ptr(rs2),
+                                                 _ptr(ind)))
+        return norm[:n], rs[:n], rs2[:n], ind[:n]
+
     def normalized_aggregate(self, row_ptr, col, x, norm, selfl, out=None):
         n = row_ptr.numel() - 1
         if out is None:

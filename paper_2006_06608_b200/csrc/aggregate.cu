@@ -159,6 +159,13 @@ struct Lanes {
     }
 };
 
+// Per-row epilogue scalars are prefetched into L1 when the row's unit starts
+// (K3), so the final store's loads hit L1 instead of trailing the gather by
+// an L2 round trip; no registers are held across the gather.
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <class T, int VEC, bool FAN = false>
 __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32_t off, Vec<T, VEC> val) {
     T* y = static_cast<T*>(a.y) + (size_t)v * a.dim + off;
@@ -307,6 +314,10 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(Ag
         e = __ldg(a.part_ptr + u + 1);
         v = __ldg(a.part2node + u);
         f = __ldg(a.uflags + u);
+    }
+    if (active && a.epi) {
+        if (a.epi & EPI_SCALE) prefetch_l1(a.scale + v);
+        if ((a.epi & EPI_SELF) && a.sw) prefetch_l1(a.sw + v);
     }
     const bool direct = (f & (UF_LEADER | UF_RUN_END)) == (UF_LEADER | UF_RUN_END) && !(f & UF_SPLIT);
     const bool staged = active && !direct;

@@ -92,6 +92,17 @@ __global__ void k5_gcn_node_weights(uint32_t n, const double* __restrict__ norm,
     }
 }
 
+// Folded-normalisation operands (gnna_gcn_fold_weights): thread per node.
+__global__ void k5_gcn_fold_weights(uint32_t n, const double* __restrict__ norm, const uint8_t* __restrict__ self,
+                                    float* __restrict__ rs, float* __restrict__ rs2, float* __restrict__ ind) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const double nv = norm[v];
+        if (rs) rs[v] = (float)nv;
+        if (rs2) rs2[v] = (float)(nv * nv);
+        if (ind) ind[v] = self[v] ? 1.f : 0.f;
+    }
+}
+
 // engine.cpp:162-172 features_close: count elements with
 // |a-b| > tol * max(|a|, |b|) (NaN compares false there, and here).
 template <class T>
@@ -204,17 +215,22 @@ struct TransientPlan {
 // D^-1/2 (A [+I]) D^-1/2 from the forward CSR's degrees; node-indexed, so the
 // same arrays serve the forward CSR and its transpose (the adjoint).
 struct GcnWeights {
-    DevBuf<float> rs, sw;
+    DevBuf<float> rs, sw, ind;  // ind: the folded form's self indicator (fwd constructor only)
+    DevBuf<double> norm;         // the update GEMM's row-scale epilogue (fwd constructor only)
     GcnWeights(gnna_ctx* ctx, const uint64_t* fwd_rp, const uint32_t* fwd_col, uint32_t n, int add_self) {
         rs = DevBuf<float>(n ? n : 1, ctx->stream);
         sw = DevBuf<float>(n ? n : 1, ctx->stream);
+        ind = DevBuf<float>(n ? n : 1, ctx->stream);
+        norm = DevBuf<double>(n ? n : 1, ctx->stream);
         if (!n) return;
-        DevBuf<double> norm(n, ctx->stream);
         DevBuf<uint8_t> self(n, ctx->stream);
         gcn_norm(ctx, fwd_rp, fwd_col, n, add_self, norm.get(), self.get());
         k5_gcn_node_weights<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(n, norm.get(), self.get(), rs.get(),
                                                                               sw.get());
         gnna::launched(ctx, "k5_gcn_node_weights");
+        k5_gcn_fold_weights<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(n, norm.get(), self.get(), nullptr,
+                                                                              nullptr, ind.get());
+        gnna::launched(ctx, "k5_gcn_fold_weights");
     }
     // from norm/self arrays the caller already holds
     GcnWeights(gnna_ctx* ctx, const double* norm, const uint8_t* self, uint32_t n) {
@@ -250,9 +266,14 @@ void fast_gcn_forward(gnna_ctx* ctx, const uint64_t* rp, const uint32_t* col, ui
     TransientPlan plan(ctx, rp, col, n, std::min(in_dim, out_dim));
     GcnWeights gw(ctx, rp, col, n, add_self);
     if (out_dim < in_dim) {
+        // folded normalisation: t' = norm * (X W) in the GEMM epilogue, then
+        // y = norm * (A t' + self * t'), a plain-sum K3 (no per-edge gather)
         DevBuf<float> t((size_t)n * out_dim, ctx->stream);
-        gnna::gemm(ctx, GNNA_F32, x, n, in_dim, w, out_dim, nullptr, 0, nullptr, t.get());
-        const gnna_agg_opts o = gw.opts(out_dim);
+        gnna::gemm(ctx, GNNA_F32, x, n, in_dim, w, out_dim, nullptr, 2, gw.norm.get(), t.get());
+        gnna_agg_opts o{};
+        o.dim = out_dim;
+        o.self_weight = add_self ? gw.ind.get() : nullptr;  // no implicit self loops: no self term
+        o.row_scale = gw.rs.get();
         gnna::aggregate_plan_ex(ctx, plan.p, GNNA_F32, GNNA_DIM_CYCLIC, t.get(), y, &o);
     } else {
         DevBuf<float> z((size_t)n * in_dim, ctx->stream);
@@ -324,6 +345,22 @@ gnna_status gnna_gcn_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
         k5_gcn_weights<<<gnna::grid_for((uint64_t)n * 32, 256), 256, 0, ctx->stream>>>(
             d_row_ptr, d_col, n, norm.get(), self.get(), d_row_scale, d_self_weight, d_edge_weight);
         gnna::launched(ctx, "k5_gcn_weights");
+    });
+}
+
+gnna_status gnna_gcn_fold_weights(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                                  int add_self_loops, double* d_norm, float* d_row_scale, float* d_row_scale2,
+                                  float* d_self_ind) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (!n) return;
+        DevBuf<double> tmp(d_norm ? 1 : n, ctx->stream);
+        double* norm = d_norm ? d_norm : tmp.get();
+        DevBuf<uint8_t> self(n, ctx->stream);
+        gcn_norm(ctx, d_row_ptr, d_col, n, add_self_loops, norm, self.get());
+        k5_gcn_fold_weights<<<gnna::grid_for(n, 256), 256, 0, ctx->stream>>>(n, norm, self.get(), d_row_scale,
+                                                                              d_row_scale2, d_self_ind);
+        gnna::launched(ctx, "k5_gcn_fold_weights");
     });
 }
 

@@ -38,6 +38,12 @@ class GCN2:
         # one schedule (K1 units + K2 Algorithm-1 plan) for every aggregation of the step
         self.plan = ctx.plan(row_ptr, col, params, WARP_SHARED)
         self.rs, self.sw, _ = ctx.gcn_weights(row_ptr, col, self_loops, edge_weights=False)
+        # folded form: the source-side D^-1/2 rides in the producing GEMM's
+        # row-scale epilogue (norm), or in the previous aggregation's epilogue
+        # (norm^2), so those aggregations are plain sums (no per-edge gather)
+        self.norm, _, self.rs2, self.ind = ctx.gcn_fold_weights(row_ptr, col, self_loops)
+        if not self_loops:  # no implicit self loops: the self term is identically zero
+            self.sw = self.ind = None
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
         self.w1 = ((torch.rand((in_dim, hidden), generator=g, device=dev) * 2 - 1) / math.sqrt(in_dim)).contiguous()
@@ -47,24 +53,35 @@ class GCN2:
         self.lr = lr
 
     def _agg(self, x, relu=False, mask=None, out=None):
+        """Â x for an x nobody pre-scaled: K3 gathers norm[u] per edge."""
         return self.plan.aggregate_ex(x, out=out, node_weight=self.rs, self_weight=self.sw, row_scale=self.rs,
                                       relu=relu, mask=mask)
+
+    def _aggf(self, xs, scale, relu=False, mask=None, out=None):
+        """Â x given xs = norm * x (pre-scaled by its producer): a plain-sum K3
+        with the destination scale (norm, or norm^2 when the result feeds
+        another aggregation) and the self term in the epilogue."""
+        return self.plan.aggregate_ex(xs, out=out, self_weight=self.ind, row_scale=scale, relu=relu, mask=mask)
 
     def forward(self, x):
         ctx = self.ctx
         in_dim, hid, out_dim = self.dims
         s = {}
+        agg2_first = out_dim >= hid  # layer 2 aggregates first (then h1 feeds an aggregation)
         if hid < in_dim:  # layer 1 update first: h1 = relu(Â (x W1))
-            s["t1"] = ctx.gemm(x, self.w1)
-            s["h1"] = self._agg(s["t1"], relu=True)
+            s["t1"] = ctx.gemm(x, self.w1, None, 2, self.norm)  # norm * (x W1)
+            # relu(norm^2 * S) = norm * relu(norm * S): h1 comes out pre-scaled for layer 2
+            s["h1"] = self._aggf(s["t1"], self.rs2 if agg2_first else self.rs, relu=True)
+            s["h1_scaled"] = agg2_first
         else:  # aggregate first: h1 = relu((Â x) W1)
             s["z1"] = self._agg(x)
             s["h1"] = ctx.gemm(s["z1"], self.w1, self.zero_b1, 1)
-        if out_dim < hid:  # layer 2 update first
-            s["t2"] = ctx.gemm(s["h1"], self.w2)
-            y = self._agg(s["t2"])
+            s["h1_scaled"] = False
+        if not agg2_first:  # layer 2 update first
+            s["t2"] = ctx.gemm(s["h1"], self.w2, None, 2, self.norm)
+            y = self._aggf(s["t2"], self.rs)
         else:
-            s["z2"] = self._agg(s["h1"])
+            s["z2"] = self._aggf(s["h1"], self.rs) if s["h1_scaled"] else self._agg(s["h1"])
             y = ctx.gemm(s["z2"], self.w2)
         self.saved = s
         return y
@@ -80,12 +97,16 @@ class GCN2:
             dw2 = ctx_gemm_tn(ctx, s["h1"], dt2)                   # h1^T dT2
             dh1 = ctx.gemm(dt2, w2t)
             dp1 = dh1 * (s["h1"] > 0)
+            dp1_scaled = False
         else:
             dw2 = ctx_gemm_tn(ctx, s["z2"], dy)                    # (Â h1)^T dY
-            dz2 = ctx.gemm(dy, w2t)                                # dY W2^T
-            dp1 = self._agg(dz2, mask=s["h1"])                     # Â^T dZ2, masked by relu'(h1)
+            dz2 = ctx.gemm(dy, w2t, None, 2, self.norm)            # norm * (dY W2^T)
+            # Â^T dZ2 masked by relu'(h1) (the sign of a pre-scaled h1 is the same);
+            # pre-scaled by norm again when the next aggregation consumes it
+            dp1_scaled = hid < in_dim
+            dp1 = self._aggf(dz2, self.rs2 if dp1_scaled else self.rs, mask=s["h1"])
         if hid < in_dim:
-            dt1 = self._agg(dp1)                                   # Â^T dP1
+            dt1 = self._aggf(dp1, self.rs) if dp1_scaled else self._agg(dp1)  # Â^T dP1
             dw1 = ctx_gemm_tn(ctx, x, dt1)                         # x^T dT1
         else:
             dw1 = ctx_gemm_tn(ctx, s["z1"], dp1)
