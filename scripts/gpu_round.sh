@@ -14,6 +14,7 @@ for w in c5 c3; do
   ncu -i /tmp/k3_${w}_$R.ncu-rep --page source --csv > gpurun_out/k3_${w}_${R}_source.csv 2>/dev/null
 done
 for w in c1 c2 c3 c4; do timeout 600 python bench.py --workload $w --steps 20 --warmup 5 --no-e2e 2>/dev/null | tail -1; done > gpurun_out/sweep_$R.jsonl
+timeout 600 python bench.py --workload c3 --agg gcn --steps 20 --warmup 5 --no-e2e 2>/dev/null | tail -1 > gpurun_out/c3gcn_$R.json
 timeout 600 python bench.py --workload c3train --steps 20 --warmup 5 2>/dev/null | tail -1 > gpurun_out/c3train_$R.json
 timeout 300 python scripts/gemm_ab.py > gpurun_out/gemm_ab_$R.jsonl 2>&1
 GNNA_GEMM_SIMT=1 timeout 300 python scripts/gemm_ab.py > gpurun_out/gemm_ab_simt_$R.jsonl 2>&1
