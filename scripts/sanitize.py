@@ -60,6 +60,25 @@ def main():
     ctx.apply_mapping_csr(drp, dcol, o2n, n2o)
     m = GCN2(ctx, drp, dcol, 24, 16, 8)
     m.step(dev(x).float(), dev(rng.random((n, 8))).float())
+    # tcgen05 GEMMs: TMA-fed (k % 4 == 0), register-fed (k = 22), both dW kernels, fused epilogues
+    from paper_2006_06608_b200.gcn import ctx_gemm_tn
+    for k, q in ((96, 16), (22, 16), (16, 22), (64, 64)):
+        a = dev(rng.random((n, k)) - 0.5).float()
+        wq = dev(rng.random((k, q)) - 0.5).float()
+        g = dev(rng.random((n, q)) - 0.5).float()
+        want = a.double() @ wq.double()
+        assert torch.allclose(ctx.gemm(a, wq).double(), want, rtol=1e-4, atol=1e-4)
+        ctx.gemm(a, wq, dev(rng.random(q)).float(), 1)
+        ctx.gemm(a, wq, None, 2, dev(rng.random(n)))
+        assert torch.allclose(ctx_gemm_tn(ctx, a, g).double(), a.double().t() @ g.double(), rtol=1e-4, atol=1e-3)
+    # fused all-gather: K3 fan-out into local replicas
+    p = Params.make(ngs=16, dw=16, tpb=256, dim=32)
+    plan = ctx.plan(drp, dcol, p, 2, rows=(100, 2500))
+    xf = dev(rng.random((n, 32))).float()
+    y = torch.zeros((n, 32), device="cuda")
+    reps = [torch.zeros((n, 32), device="cuda") for _ in range(3)]
+    plan.aggregate_fanout(xf, y, peers=reps)
+    assert all(torch.equal(r, y) for r in reps)
     torch.cuda.synchronize()
     print("sanitize workload ok")
 
