@@ -601,6 +601,22 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
     const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_cta;
     const uint64_t r_end = r_begin + rows_per_cta < m ? r_begin + rows_per_cta : m;
     const uint32_t nblk = r_end > r_begin ? (uint32_t)((r_end - r_begin + TS_BK - 1) / TS_BK) : 0u;
+    // one contiguous run of floats: 16-byte cp.async where both ends are
+    // 16-byte aligned (shared tiles are), 4-byte for the head/tail remainder
+    auto copy_run = [&](float* dst, const float* src, uint32_t cnt) {
+        const uint32_t head = (uint32_t)((16 - ((uintptr_t)src & 15)) & 15) / 4;
+        const bool v16 = (((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0 && cnt > head;
+        const uint32_t h = v16 ? head : cnt;
+        for (uint32_t e = t; e < h; e += blockDim.x) cp_async4(dst + e, src + e);
+        if (!v16) return;
+        const uint32_t nv = (cnt - h) / 4;
+        for (uint32_t e = t; e < nv; e += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(dst + h + 4 * e)),
+                         "l"(src + h + 4 * e)
+                         : "memory");
+        for (uint32_t e = h + 4 * nv + t; e < cnt; e += blockDim.x) cp_async4(dst + e, src + e);
+    };
     auto load = [&](uint32_t blk, uint32_t buf) {
         const uint64_t r0 = r_begin + (uint64_t)blk * TS_BK;
         const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)TS_BK ? r_end - r0 : (uint64_t)TS_BK);
@@ -608,8 +624,8 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
         const float* gb = b + r0 * q;
         float* da = sa + (size_t)buf * TS_BK * p;
         float* db = sb + (size_t)buf * TS_BK * q;
-        for (uint32_t e = t; e < nr * p; e += blockDim.x) cp_async4(da + e, ga + e);
-        for (uint32_t e = t; e < nr * q; e += blockDim.x) cp_async4(db + e, gb + e);
+        copy_run(da, ga, nr * p);
+        copy_run(db, gb, nr * q);
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     float acc[TI][TJ];
@@ -632,6 +648,7 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
         if (active) {
             const float* xa = sa + (size_t)buf * TS_BK * p;
             const float* xb = sb + (size_t)buf * TS_BK * q;
+#pragma unroll 4
             for (uint32_t k = grp; k < nr; k += rg) {
                 float av[TI], bv[TJ];
 #pragma unroll
@@ -798,7 +815,7 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
     }
     if constexpr (std::is_same<T, float>::value) {
         if (gnna::gemm_tn_tc_f32(ctx, a, b, m, p, q, out)) return;
-        constexpr uint32_t TI = 2, TJ = 4;
+        constexpr uint32_t TI = 4, TJ = 4;
         const uint32_t tiles = ((p + TI - 1) / TI) * ((q + TJ - 1) / TJ);
         const size_t sbytes = std::max<size_t>((size_t)2 * TS_BK * (p + q), (size_t)(256 / std::max(tiles, 1u)) * p * q) * 4;
         static const bool no_small = std::getenv("GNNA_TN_WARP") != nullptr;  // A/B switch
