@@ -129,7 +129,8 @@ def dense_norm_adj(rp, col, self_loops):
     return d[:, None] * A * d[None, :]
 
 
-@pytest.mark.parametrize("dims,sl", [((96, 16, 22), False), ((12, 32, 8), True), ((20, 16, 16), False)])
+@pytest.mark.parametrize("dims,sl", [((96, 16, 22), False), ((12, 32, 8), True), ((20, 16, 16), False),
+                                     ((24, 16, 16), True), ((40, 16, 8), True), ((24, 16, 8), False)])
 def test_gcn2_step_vs_autograd_and_reference(ctx, orc, dims, sl):
     from paper_2006_06608_b200.gcn import GCN2
     rng = np.random.default_rng(sum(dims))
