@@ -114,7 +114,8 @@ struct TcArgs {
     uint32_t m, k, n;
     int epilogue;  // 0 none, 1 bias + relu, 2 row scale
     uint32_t tiles;
-    int vec;  // A rows are float4-loadable (k % 4 == 0, 16-byte aligned)
+    int vec;   // A rows are float4-loadable (k % 4 == 0, 16-byte aligned)
+    int vec2;  // A rows are float2-loadable (k % 2 == 0, 8-byte aligned)
 };
 
 template <int KP, int NP>
@@ -171,6 +172,15 @@ __global__ void __launch_bounds__(TM) k6_gemm_tc(TcArgs g) {
 #pragma unroll
             for (int c = 0; c < KC; ++c)
                 v[c] = (row < g.m && (uint32_t)c * 4 < g.k) ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        } else if (g.vec2) {  // even k, 8-byte aligned rows: half the load instructions
+            const float2* src = reinterpret_cast<const float2*>(g.a + row * g.k);
+#pragma unroll
+            for (int c = 0; c < KC; ++c) {
+                const uint32_t kk = (uint32_t)c * 4;
+                const float2 lo2 = (row < g.m && kk < g.k) ? __ldg(src + 2 * c) : make_float2(0.f, 0.f);
+                const float2 hi2 = (row < g.m && kk + 2 < g.k) ? __ldg(src + 2 * c + 1) : make_float2(0.f, 0.f);
+                v[c] = make_float4(lo2.x, lo2.y, hi2.x, hi2.y);
+            }
         } else {
             const float* src = g.a + row * g.k;
 #pragma unroll
@@ -904,7 +914,7 @@ bool gemm_tc_f32(gnna_ctx* ctx, const float* a, const float* w, const float* bia
                  float* out, uint32_t m, uint32_t k, uint32_t n, int epilogue) {
     if (k == 0 || k > 128 || m == 0 || n == 0) return false;
     TcArgs g{a, w, bias, row_scale, out, m, k, n, epilogue, (m + TM - 1) / TM,
-             (k % 4 == 0 && ((uintptr_t)a % 16 == 0)) ? 1 : 0};
+             (k % 4 == 0 && ((uintptr_t)a % 16 == 0)) ? 1 : 0, (k % 2 == 0 && ((uintptr_t)a % 8 == 0)) ? 1 : 0};
     static const bool no_tma = std::getenv("GNNA_GEMM_TC_LD") != nullptr;  // A/B switch
     if (g.vec && !no_tma) {
         const bool ok = k <= 32 ? launch_tma_n<32>(ctx, g)
