@@ -583,10 +583,38 @@ def run_e2e(ctx, rp, col, x, p, r0, r1, cfg, args, world, dev):
     nnz = int(col.numel())
     h2d = h_rp.numel() * 8 + h_col.numel() * 4 + h_x.numel() * 4
     d2h = h_y.numel() * 4
+    duplex = pcie_duplex_gbps()
+    floor_ms = (h2d + d2h) / (duplex * 1e9) * 1e3 if duplex else None
     return {"value": nnz * cfg.dim / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": t * 1e3, "steps": steps, "single_call_ms": single * 1e3,
+            "pcie_duplex_GBps_measured": duplex, "pcie_floor_ms_per_step": floor_ms,
             "path": "gnna_aggregate_host_stream (C-ABI, pinned host buffers; per batch: CSR slice + features "
                     "upload, plan, K3, rows download; batches pipelined)"}
+
+
+def pcie_duplex_gbps(gb=1):
+    """Measured full-duplex pinned copy bandwidth (H2D and D2H at once on two
+    streams, GB/s total): the floor of the e2e step, whose copies overlap."""
+    import torch
+    try:
+        n = gb * (1 << 30) // 4
+        h, h2 = torch.empty(n).pin_memory(), torch.empty(n).pin_memory()
+        d, d2 = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def both():
+            with torch.cuda.stream(s1):
+                d.copy_(h, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h2.copy_(d2, non_blocking=True)
+        both()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        both()
+        torch.cuda.synchronize()
+        return round(2 * n * 4 / (time.perf_counter() - t0) / 1e9, 1)
+    except Exception:
+        return None
 
 
 def run_train(args):
