@@ -36,6 +36,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -556,6 +557,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
 }
 
+// cudaFuncSetAttribute is per device: each kernel instance remembers the
+// devices it was configured on (one bit per device ordinal).
+template <class K>
+void smem_attr_once(std::atomic<uint64_t>& done, K kern, int device, size_t bytes) {
+    const uint64_t bit = 1ull << (device & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    done.fetch_or(bit, std::memory_order_release);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* p = nullptr;
@@ -583,11 +594,8 @@ bool launch_tc_tma(gnna_ctx* ctx, const TcArgs& g) {
         return false;
     using C = TmaCfg<KP, NP>;
     auto kern = k6_gemm_tc_tma<KP, NP>;
-    static bool attr = [&] {
-        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<uint64_t> attr{0};
+    smem_attr_once(attr, kern, ctx->device, C::SMEM);
     const uint32_t cols = (g.n + NP - 1) / NP;
     const uint32_t slots = (uint32_t)ctx->num_sms / cols;
     dim3 grid(g.tiles < slots ? g.tiles : (slots ? slots : 1), cols);
@@ -609,8 +617,9 @@ void launch_tc(gnna_ctx* ctx, const TcArgs& g0) {
     TcArgs g = g0;
     constexpr size_t smem = (size_t)2 * (KP / 4) * TM * 16 + (size_t)2 * (KP / 4) * NP * 16;
     auto kern = k6_gemm_tc<KP, NP>;
+    static std::atomic<uint64_t> attr{0};
+    smem_attr_once(attr, kern, ctx->device, smem);
     static int per_sm = [&] {
-        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int b = 0;
         GNNA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, TM, smem));
         return b < 1 ? 1 : b;
@@ -887,11 +896,8 @@ bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uin
         return false;
     using C = TnCfg<PS, QS>;
     auto kern = k6_gemm_tn_tc<PS, QS>;
-    static bool attr = [&] {
-        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-        return true;
-    }();
-    (void)attr;
+    static std::atomic<uint64_t> attr{0};
+    smem_attr_once(attr, kern, ctx->device, C::SMEM);
     const uint32_t nblk = (m + TN_BK - 1) / TN_BK;
     uint32_t ctas = nblk < (uint32_t)ctx->num_sms ? nblk : (uint32_t)ctx->num_sms;
     const uint32_t bpc = (nblk + ctas - 1) / ctas;
