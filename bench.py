@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--flush-l2", action="store_true", help="force an L2 flush between steps")
     ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gin"],
                     help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized), gin (sum + (1+eps)x)")
+    ap.add_argument("--no-l2-pin", action="store_true", help="do not pin the hub rows of x in L2")
     ap.add_argument("--multimem", action="store_true",
                     help="N > 1: fused gather through the NVLS multicast address (multimem.st) instead of P2P stores")
     ap.add_argument("--nccl-gather", action="store_true",
@@ -362,6 +363,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     plan_s = time.time() - t1
 
+    # L2 residency for the hub rows (gnna_set_l2_window), only when the front
+    # rows carry a disproportionate share of the gathers
+    l2_pin = ctx.pin_hot_rows(rp_host, x) if not args.no_l2_pin else {"pinned": False, "disabled": True}
+
     x_bytes = x.numel() * 4
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = args.flush_l2 or x_bytes < 4 * l2
@@ -427,6 +432,8 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
     launches = ctx.launches - launches0
+    if l2_pin.get("pinned"):
+        ctx.set_l2_window(None, 0)  # the e2e and side measurements run on other buffers
     step_ms = [a.elapsed_time(c) for a, _, c in ev]
     agg_ms = [a.elapsed_time(b) for a, b, _ in ev]
     t_step = sum(step_ms) / len(step_ms)
@@ -494,6 +501,7 @@ def run_ours(args):
                                        "gcn": "GCN normalized_aggregate D^-1/2 A D^-1/2 x (fused)",
                                        "gin": "GIN sum + (1+eps) x, eps 0.1 (fused)"}[args.agg],
                        "l2": "flushed between steps" if flush else f"inputs ({x_bytes / 1e9:.2f} GB x) > L2 ({l2 / 1e6:.0f} MB)",
+                       "l2_window": l2_pin,
                        "plan": plan.info(), "graph_build_s": round(gen_s, 3), "plan_build_s": round(plan_s, 3),
                        "max_degree": int(np.diff(rp_host).max())},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -80,6 +80,15 @@ GNNA_API gnna_status gnna_set_stream(gnna_ctx* ctx, void* cuda_stream);
 GNNA_API void* gnna_get_stream(const gnna_ctx* ctx);
 GNNA_API gnna_status gnna_synchronize(gnna_ctx* ctx);
 GNNA_API const char* gnna_last_error(const gnna_ctx* ctx);
+/* L2 residency for the gather's hot rows (B200: 126 MB L2).  Marks
+ * [base, base + bytes) as an access-policy window on the context's stream:
+ * hits persist in a set-aside L2 region (sized to the window, capped at the
+ * device's persisting maximum), misses stream.  With rows numbered by
+ * descending degree (the power-law hubs first), the window holds the rows
+ * the aggregation re-reads most.  bytes == 0 clears the window and resets the
+ * persisting lines.  *applied (may be NULL) receives the window size used. */
+GNNA_API gnna_status gnna_set_l2_window(gnna_ctx* ctx, const void* base, uint64_t bytes, double hit_ratio,
+                                        uint64_t* applied);
 GNNA_API const char* gnna_version(void);
 /* Number of kernels this library has launched on ctx (for bench.py). */
 GNNA_API uint64_t gnna_launch_count(const gnna_ctx* ctx);

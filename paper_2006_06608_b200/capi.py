@@ -166,6 +166,40 @@ class Context:
     def synchronize(self):
         self._check(self.L.gnna_synchronize(self.h))
 
+    def pin_hot_rows(self, row_ptr_host, x, cap_bytes=48 << 20, min_gain=4.0):
+        """Data-driven L2 residency for the gather (gnna_set_l2_window): when
+        the front rows of x (what fits in cap_bytes) receive at least
+        min_gain times their uniform share of the gathers -- power-law hubs
+        numbered first -- pin them; otherwise leave L2 alone.  The gather
+        share of rows [0, k) is row_ptr[k] / nnz (symmetric CSR: in-degree =
+        degree).  Inputs smaller than L2 are never pinned.  Returns a dict for
+        the bench's config."""
+        rp = np.asarray(row_ptr_host).view(np.uint64) if np.asarray(row_ptr_host).dtype != np.uint64 else \
+            np.asarray(row_ptr_host)
+        n, nnz = len(rp) - 1, int(rp[-1])
+        row_bytes = x.shape[1] * x.element_size()
+        l2 = self.torch.cuda.get_device_properties(x.device).L2_cache_size
+        info = {"pinned": False, "cap_MB": cap_bytes >> 20}
+        if n == 0 or nnz == 0 or x.numel() * x.element_size() <= l2:
+            return info
+        k = min(n, cap_bytes // row_bytes)
+        share = float(rp[k]) / nnz
+        uniform = k / n
+        info.update({"rows": int(k), "gather_share": round(share, 4), "uniform_share": round(uniform, 6)})
+        if share >= min_gain * uniform:
+            info["applied_bytes"] = self.set_l2_window(x, k * row_bytes, 1.0)
+            info["pinned"] = True
+        return info
+
+    def set_l2_window(self, base=None, nbytes=0, hit_ratio=1.0):
+        """gnna_set_l2_window: persist [base, base+nbytes) in L2 on this
+        context's stream (base: tensor or pointer); nbytes 0 clears it."""
+        ptr = 0 if base is None else (base if isinstance(base, int) else base.data_ptr())
+        applied = C.c_uint64()
+        self._check(self.L.gnna_set_l2_window(self.h, C.c_void_p(ptr), C.c_uint64(int(nbytes)),
+                                              C.c_double(hit_ratio), C.byref(applied)))
+        return applied.value
+
     def _empty(self, n, dtype):
         return self.torch.empty(n, dtype=dtype, device=f"cuda:{self.device}")
 

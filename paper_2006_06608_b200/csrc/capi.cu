@@ -68,6 +68,36 @@ gnna_status gnna_synchronize(gnna_ctx* ctx) {
 
 const char* gnna_last_error(const gnna_ctx* ctx) { return ctx ? ctx->err.c_str() : "null gnna_ctx"; }
 
+gnna_status gnna_set_l2_window(gnna_ctx* ctx, const void* base, uint64_t bytes, double hit_ratio,
+                               uint64_t* applied) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (hit_ratio < 0.0 || hit_ratio > 1.0) gnna::raise(GNNA_ERR_DOMAIN, "set_l2_window: hit_ratio in [0, 1]");
+        cudaStreamAttrValue v{};
+        if (!bytes || !base) {
+            v.accessPolicyWindow.num_bytes = 0;
+            GNNA_CUDA(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+            GNNA_CUDA(cudaCtxResetPersistingL2Cache());
+            GNNA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+            if (applied) *applied = 0;
+            return;
+        }
+        int max_persist = 0, max_window = 0;
+        GNNA_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+        GNNA_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+        const uint64_t win = std::min<uint64_t>(bytes, (uint64_t)std::max(0, max_window));
+        const uint64_t carve = std::min<uint64_t>(win, (uint64_t)std::max(0, max_persist));
+        GNNA_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+        v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+        v.accessPolicyWindow.num_bytes = win;
+        v.accessPolicyWindow.hitRatio = (float)hit_ratio;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        GNNA_CUDA(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v));
+        if (applied) *applied = win;
+    });
+}
+
 uint64_t gnna_launch_count(const gnna_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 gnna_status gnna_device_alloc(gnna_ctx* ctx, size_t bytes, void** out) {
