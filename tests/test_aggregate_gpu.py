@@ -225,3 +225,23 @@ def test_plan_info_runs_and_units(ctx, orc):
         _, _, lead, _ = orc.build_mem_plan(tg, P(**kw).tolist()) if len(tg) else (None, None, np.zeros(0), 0)
         info = ctx.plan(*to_dev(rp, col), P(**kw), 2).info()
         assert info["groups"] == len(tg) and info["runs"] == int(np.sum(lead)), (t, info)
+
+
+def test_l2_window_keeps_results(ctx, orc):
+    """gnna_set_l2_window is a residency hint only: the pinned run is bit-identical."""
+    import torch
+    from paper_2006_06608_b200.capi import Params
+    rng = np.random.default_rng(8)
+    n = 4000
+    rp, col, _ = random_graph(rng, n, 30000, orc=orc)
+    drp, dcol = to_dev(rp, col)
+    x = to_dev(rng.random((n, 64)))
+    plan = ctx.plan(drp, dcol, Params.make(ngs=16, dw=16, tpb=256, dim=64), 2)
+    want = plan.aggregate(x).clone()
+    applied = ctx.set_l2_window(x, 1 << 20, 1.0)
+    assert 0 < applied <= 1 << 20
+    assert torch.equal(plan.aggregate(x), want)
+    assert ctx.set_l2_window(None, 0) == 0
+    assert torch.equal(plan.aggregate(x), want)
+    # x smaller than L2: the data-driven pin leaves L2 alone
+    assert ctx.pin_hot_rows(rp, x)["pinned"] is False
