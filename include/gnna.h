@@ -354,6 +354,13 @@ GNNA_API gnna_status gnna_modularity(gnna_ctx* ctx, const uint64_t* d_row_ptr, c
 GNNA_API gnna_status gnna_build_mapping(gnna_ctx* ctx, const uint32_t* d_com, uint32_t n,
                                uint32_t num_communities, uint32_t* d_old_to_new,
                                uint32_t* d_new_to_old);
+/* Degree order (B200 addition, no reference counterpart): new ids by
+ * descending degree, ties by old id.  Numbering the power-law hubs first
+ * makes them one contiguous front block of the feature matrix, which
+ * gnna_set_l2_window can keep resident in L2.  Apply with
+ * gnna_apply_mapping_csr and a row gather of the features. */
+GNNA_API gnna_status gnna_degree_order(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
+                                       uint32_t* d_old_to_new, uint32_t* d_new_to_old);
 /* renumber.cpp:148 mapping_from_vector (DOMAIN if not a permutation). */
 GNNA_API gnna_status gnna_mapping_from_vector(gnna_ctx* ctx, const uint32_t* d_vec, uint32_t n,
                                      uint32_t* d_old_to_new, uint32_t* d_new_to_old);

@@ -442,6 +442,13 @@ class Context:
                                            _ptr(com), C.c_uint32(ncom), C.byref(q)))
         return q.value
 
+    def degree_order(self, row_ptr):
+        """gnna_degree_order: (old_to_new, new_to_old) by descending degree, ties by id."""
+        n = row_ptr.numel() - 1
+        o2n, n2o = self._empty(max(n, 1), self.torch.int32), self._empty(max(n, 1), self.torch.int32)
+        self._check(self.L.gnna_degree_order(self.h, _ptr(row_ptr), C.c_uint32(n), _ptr(o2n), _ptr(n2o)))
+        return o2n[:n], n2o[:n]
+
     def build_mapping(self, com, ncom):
         n = com.numel()
         o2n, n2o = self._empty(max(n, 1), self.torch.int32), self._empty(max(n, 1), self.torch.int32)

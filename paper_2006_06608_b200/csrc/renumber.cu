@@ -85,6 +85,16 @@ __global__ void k7_mapping_keys(const uint32_t* __restrict__ com, uint32_t n, ui
     }
 }
 
+// Degree order (the L2-residency renumbering): key = (~deg << 32) | id, so an
+// ascending sort gives descending degree, ties by id.
+__global__ void k7_degree_keys(const uint64_t* __restrict__ row_ptr, uint32_t n, uint64_t* __restrict__ keys) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t d = row_ptr[v + 1] - row_ptr[v];
+        const uint32_t dc = d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d;
+        keys[v] = ((uint64_t)(~dc) << 32) | v;
+    }
+}
+
 __global__ void k7_mapping_scatter(const uint64_t* __restrict__ keys, uint32_t n, uint32_t* __restrict__ o2n,
                                    uint32_t* __restrict__ n2o) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -227,6 +237,21 @@ gnna_status gnna_build_mapping(gnna_ctx* ctx, const uint32_t* d_com, uint32_t n,
         k7_mapping_scatter<<<gnna::grid_for(n, 256), 256, 0, s>>>(keys.get(), n, d_old_to_new, d_new_to_old);
         gnna::launched(ctx, "k7_mapping_scatter");
         GNNA_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+gnna_status gnna_degree_order(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n, uint32_t* d_old_to_new,
+                              uint32_t* d_new_to_old) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (!n) return;
+        cudaStream_t s = ctx->stream;
+        DevBuf<uint64_t> keys(n, s);
+        k7_degree_keys<<<gnna::grid_for(n, 256), 256, 0, s>>>(d_row_ptr, n, keys.get());
+        gnna::launched(ctx, "k7_degree_keys");
+        gnna::sort_keys_u64(ctx, keys.get(), n, 64);
+        k7_mapping_scatter<<<gnna::grid_for(n, 256), 256, 0, s>>>(keys.get(), n, d_old_to_new, d_new_to_old);
+        gnna::launched(ctx, "k7_mapping_scatter");
     });
 }
 

@@ -119,3 +119,38 @@ def test_mapping_errors(ctx):
     bad = to_dev(np.array([0, 0, 1], np.uint32))
     with pytest.raises(DomainError):
         ctx.apply_mapping_csr(rp, col, bad, bad)
+
+
+def test_degree_order_and_aggregation_equivalence(ctx, orc):
+    """gnna_degree_order: descending degree, ties by old id (bit-exact vs a
+    numpy stable sort); aggregating the renumbered graph on renumbered rows is
+    the original aggregation permuted (fp64: identical bits per row, since each
+    row's CSR order maps to the same neighbor sequence only up to the sort, so
+    compare against the oracle on the renumbered CSR)."""
+    import torch
+    from conftest import random_graph, to_dev
+    from paper_2006_06608_b200.capi import Params
+    rng = np.random.default_rng(9)
+    for n, e in ((1, 0), (50, 300), (3000, 20000)):
+        rp, col, _ = random_graph(rng, n, e, orc=orc)
+        drp, dcol = to_dev(rp, col)
+        o2n, n2o = ctx.degree_order(drp)
+        deg = np.diff(rp.astype(np.int64))
+        want_n2o = np.lexsort((np.arange(n), -deg)).astype(np.uint32)
+        assert np.array_equal(n2o.cpu().numpy().view(np.uint32), want_n2o)
+        want_o2n = np.empty(n, np.uint32)
+        want_o2n[want_n2o] = np.arange(n, dtype=np.uint32)
+        assert np.array_equal(o2n.cpu().numpy().view(np.uint32), want_o2n)
+        if e == 0:
+            continue
+        rp2, col2 = ctx.apply_mapping_csr(drp, dcol, o2n, n2o)
+        x = rng.random((n, 16))
+        x2 = x[want_n2o]
+        p = Params.make(ngs=8, dw=16, tpb=128, dim=16)
+        got = ctx.plan(rp2, col2, p, 2).aggregate(to_dev(x2)).cpu().numpy()
+        want, _ = orc.aggregate_scheduled(rp2.cpu().numpy().view(np.uint64), col2.cpu().numpy().view(np.uint32), x2,
+                                          p.tolist(), 2, 1)
+        assert np.array_equal(got, want)
+        # same sums as the original graph, row for row (to fp64 rounding of reordered adds)
+        orig, _ = orc.aggregate_scheduled(rp, col, x, p.tolist(), 2, 1)
+        np.testing.assert_allclose(got, orig[want_n2o], rtol=1e-12, atol=1e-12)
