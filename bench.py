@@ -144,10 +144,12 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def cpu_sample(cfg, n_nodes, seed_offset=0):
+def cpu_sample(cfg, n_nodes, seed_offset=0, order="natural"):
     """A bounded sample of the same workload for the CPU reference: the same
     generator and mean degree at n_nodes, canonicalised by the reference's
-    own to_csr; fp64 U[0,1) features."""
+    own to_csr; fp64 U[0,1) features.  order="degree" applies the same
+    renumbering as our arm (descending degree, ties by id) before the
+    reference's to_csr, so both arms aggregate the same workload."""
     import torch
     from oracle.cpu import Oracle
     from paper_2006_06608_b200 import synth
@@ -159,6 +161,14 @@ def cpu_sample(cfg, n_nodes, seed_offset=0):
         return rp, torch.from_numpy(col.view(np.int32))
 
     edges, rp, col = synth.build_graph(cfg, to_csr, "cpu", n=n, nnz=nnz)
+    if order == "degree":
+        deg = np.diff(np.asarray(rp, dtype=np.int64))
+        n2o = np.lexsort((np.arange(n), -deg))
+        o2n = np.empty(n, np.uint32)
+        o2n[n2o] = np.arange(n, dtype=np.uint32)
+        e = edges.numpy().astype(np.uint32) if hasattr(edges, "numpy") else np.asarray(edges, np.uint32)
+        rp, col2 = ref.to_csr(n, o2n[e], True)
+        col = torch.from_numpy(col2.view(np.int32))
     col = col.numpy().view(np.uint32)
     x = np.random.default_rng(cfg.seed + seed_offset).random((n, cfg.dim))
     return ref, rp, col, x
@@ -193,7 +203,7 @@ def run_reference(args):
         return
     cfg = synth.CONFIGS[args.workload]
     nodes = args.cpu_nodes or default_cpu_nodes(cfg)
-    ref, rp, col, x = cpu_sample(cfg, nodes)
+    ref, rp, col, x = cpu_sample(cfg, nodes, order=args.order)
     workers = os.cpu_count() or 1
     # the reference's own evaluator (decider.cpp auto_params) on the sample graph
     params = [int(v) for v in ref.auto_params(ref.model_inputs(rp, col, cfg.dim))]
@@ -207,7 +217,8 @@ def run_reference(args):
     times = [time_reference(ref, rp, col, x, params, workers, 1) for _ in range(args.steps)]
     t = sum(times) / len(times)
     value = nnz * cfg.dim / t
-    sample = f"{cfg.name} generator at n={len(rp) - 1}, nnz={nnz}, d={cfg.dim}, fp64 (reference FeatureMatrix)"
+    sample = (f"{cfg.name} generator at n={len(rp) - 1}, nnz={nnz}, d={cfg.dim}, {args.order} node order, "
+              f"fp64 (reference FeatureMatrix)")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
@@ -478,7 +489,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             nodes = args.cpu_nodes or default_cpu_nodes(cfg)
-            ref, srp, scol, sx = cpu_sample(cfg, nodes)
+            ref, srp, scol, sx = cpu_sample(cfg, nodes, order=args.order)
             workers = os.cpu_count() or 1
             reps = 3
             rparams = [int(v) for v in ref.auto_params(ref.model_inputs(srp, scol, cfg.dim))]  # decider.cpp
@@ -487,7 +498,8 @@ def run_ours(args):
             cpu = {"value": snnz * cfg.dim / ts, "unit": UNIT, "cores": workers, "kind": "reference",
                    "sample": f"reference aggregate_scheduled (WarpShared, Cyclic, fp64, workers={workers}, "
                              f"its own auto_params {rparams[:3]}) on "
-                             f"{cfg.name} generator at n={len(srp) - 1}, nnz={snnz}, d={cfg.dim}; "
+                             f"{cfg.name} generator at n={len(srp) - 1}, nnz={snnz}, d={cfg.dim}, "
+                             f"{args.order} node order; "
                              f"mean of {reps} calls ({ts:.2f} s each)"}
         except Exception as exc:  # the baseline is reported, not required
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
