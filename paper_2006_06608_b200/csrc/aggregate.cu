@@ -139,6 +139,9 @@ struct AggArgs {
     void* peers[GNNA_MAX_PEERS];
     uint32_t npeer;
     void* mc;
+    // look-ahead: CTA k prefetches into L2 the unit metadata of CTA k + pf
+    // (the CTA that takes its slot when it retires); 0 = off
+    uint32_t pf;
     // K4 exact modes
     const double* norm;
     const uint8_t* self;
@@ -164,6 +167,10 @@ struct Lanes {
 // an L2 round trip; no registers are held across the gather.
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 
 template <class T, int VEC, bool FAN = false>
@@ -318,6 +325,16 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(Ag
     if (active && a.epi) {
         if (a.epi & EPI_SCALE) prefetch_l1(a.scale + v);
         if ((a.epi & EPI_SELF) && a.sw) prefetch_l1(a.sw + v);
+    }
+    if (a.pf && threadIdx.x < 32) {  // fire-and-forget: nothing waits on these
+        const uint64_t f0 = ((uint64_t)blockIdx.x + a.pf) * a.upc;
+        if (f0 < a.units) {
+            const uint32_t l = threadIdx.x;
+            const uint64_t cnt = a.units - f0 < (uint64_t)a.upc ? a.units - f0 : (uint64_t)a.upc;
+            if ((uint64_t)l * 16 <= cnt) prefetch_l2(a.part_ptr + f0 + (uint64_t)l * 16);   // 128 B = 16 x u64
+            if ((uint64_t)l * 32 < cnt) prefetch_l2(a.part2node + f0 + (uint64_t)l * 32);  // 128 B = 32 x u32
+            if ((uint64_t)l * 128 < cnt) prefetch_l2(a.uflags + f0 + (uint64_t)l * 128);
+        }
     }
     const bool direct = (f & (UF_LEADER | UF_RUN_END)) == (UF_LEADER | UF_RUN_END) && !(f & UF_SPLIT);
     const bool staged = active && !direct;
@@ -612,6 +629,10 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
     }
     a.npeer = npeer;
     a.mc = mc;
+    {
+        static const int pf_env = std::getenv("GNNA_K3_PF") ? std::atoi(std::getenv("GNNA_K3_PF")) : -1;
+        a.pf = pf_env >= 0 ? (uint32_t)pf_env : (uint32_t)(3 * ctx->num_sms);  // ~ the resident CTAs of one wave
+    }
     if (plan->G == 0 && plan->nempty == 0) return;
     const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;
     if (grid > 0x7fffffffull) raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
