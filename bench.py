@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gin"],
                     help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized), gin (sum + (1+eps)x)")
     ap.add_argument("--no-l2-pin", action="store_true", help="do not pin the hub rows of x in L2")
+    ap.add_argument("--no-graph", action="store_true", help="c3train: launch the step eagerly instead of replaying "
+                                                                "its CUDA graph")
     ap.add_argument("--order", default="degree", choices=["degree", "natural"],
                     help="node numbering: degree order (gnna_degree_order, hubs first) or the generator's")
     ap.add_argument("--multimem", action="store_true",
@@ -682,12 +684,34 @@ def run_train(args):
         model.step(x, dy)
         scratch.fill_(1.0)
     torch.cuda.synchronize()
+    graph = None
+    if not args.no_graph:
+        # the whole step (every libgnna launch, the stream-ordered scratch
+        # allocations and the SGD update) captured once as a CUDA graph:
+        # replay removes the host's ~20 ctypes calls per step
+        cap = torch.cuda.Stream()
+        cap.wait_stream(torch.cuda.current_stream())
+        ctx.set_stream(cap)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            model.step(x, dy)
+        ctx.set_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+
+    def one_step():
+        if graph is not None:
+            graph.replay()
+        else:
+            model.step(x, dy)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = ctx.launches
     with Clocks(0) as clk:
         for a, b in ev:
             a.record()
-            model.step(x, dy)
+            one_step()
             b.record()
             scratch.fill_(1.0)  # L2 flush between steps (outside the events)
         torch.cuda.synchronize()
@@ -713,7 +737,7 @@ def run_train(args):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C3 2-layer GCN fwd+bwd+SGD (96->16->22), amazon0505-shape Chung-Lu", "n": n,
                    "nnz": nnz, "aggregation_widths": widths, "params": model.params.tolist()[:3],
-                   "l2": "flushed between steps"},
+                   "l2": "flushed between steps", "cuda_graph": not args.no_graph},
         "roofline": {"bound": "hbm", "achieved": balg / (t_agg * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": balg / (t_agg * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                      "kernel": "k3_aggregate (width 16, normalised)", "kernel_ms": t_agg,

@@ -158,3 +158,39 @@ def test_gcn2_step_vs_autograd_and_reference(ctx, orc, dims, sl):
     for got, ref in ((dw1, W1.grad), (dw2, W2.grad)):
         r = ref.numpy()
         np.testing.assert_allclose(got.double().cpu().numpy(), r, rtol=1e-3, atol=1e-4 * np.abs(r).max())
+
+
+def test_gcn2_step_cuda_graph_replay(ctx, orc):
+    """The whole training step (libgnna launches through the C-ABI, their
+    stream-ordered scratch, the SGD update) captures into a CUDA graph, and
+    replays are bit-identical to eager steps (deterministic kernels)."""
+    from paper_2006_06608_b200.gcn import GCN2
+    rng = np.random.default_rng(3)
+    n = 900
+    rp, col = powerlaw_graph(orc, rng, n, 4000)
+    drp, dcol = to_dev(rp, col)
+    x = to_dev((rng.random((n, 48)) - 0.5).astype(np.float32))
+    dy = to_dev((rng.random((n, 10)) - 0.5).astype(np.float32))
+    eager = GCN2(ctx, drp, dcol, 48, 16, 10, lr=0.05)
+    graphed = GCN2(ctx, drp, dcol, 48, 16, 10, lr=0.05)
+    assert torch.equal(eager.w1, graphed.w1) and torch.equal(eager.w2, graphed.w2)
+    graphed.step(x, dy)  # warm-up (plans, attributes), then undo its update
+    graphed.w1.copy_(eager.w1)
+    graphed.w2.copy_(eager.w2)
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    ctx.set_stream(cap)
+    g = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.graph(g, stream=cap):
+            graphed.step(x, dy)
+    finally:
+        ctx.set_stream(torch.cuda.current_stream())
+    graphed.w1.copy_(eager.w1)  # capture does not execute; keep both at the same start
+    graphed.w2.copy_(eager.w2)
+    for _ in range(3):
+        g.replay()
+        eager.step(x, dy)
+    torch.cuda.synchronize()
+    assert torch.equal(graphed.w1, eager.w1) and torch.equal(graphed.w2, eager.w2)
