@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gin"],
                     help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized), gin (sum + (1+eps)x)")
     ap.add_argument("--no-l2-pin", action="store_true", help="do not pin the hub rows of x in L2")
+    ap.add_argument("--side-stream", action="store_true",
+                    help="c3train: dW2 on a second stream (measured slower: 0.464 vs 0.440 ms, kernels contend)")
     ap.add_argument("--no-graph", action="store_true", help="c3train: launch the step eagerly instead of replaying "
                                                                 "its CUDA graph")
     ap.add_argument("--order", default="degree", choices=["degree", "natural"],
@@ -673,7 +675,7 @@ def run_train(args):
     _, rp, col = synth.build_graph(cfg, lambda n, e: ctx.to_csr(n, e, True), dev)
     n, nnz = cfg.n, int(col.numel())
     in_dim, hid, out_dim = 96, 16, 22
-    model = GCN2(ctx, rp, col, in_dim, hid, out_dim, self_loops=False)
+    model = GCN2(ctx, rp, col, in_dim, hid, out_dim, self_loops=False).use_side_stream(args.side_stream)
     g = torch.Generator(device=dev)
     g.manual_seed(6)
     x = synth.features(n, in_dim, cfg.seed, dev)
@@ -737,7 +739,8 @@ def run_train(args):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": "C3 2-layer GCN fwd+bwd+SGD (96->16->22), amazon0505-shape Chung-Lu", "n": n,
                    "nnz": nnz, "aggregation_widths": widths, "params": model.params.tolist()[:3],
-                   "l2": "flushed between steps", "cuda_graph": not args.no_graph},
+                   "l2": "flushed between steps", "cuda_graph": not args.no_graph,
+                   "side_stream_dW2": bool(args.side_stream)},
         "roofline": {"bound": "hbm", "achieved": balg / (t_agg * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": balg / (t_agg * 1e-3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
                      "kernel": "k3_aggregate (width 16, normalised)", "kernel_ms": t_agg,

@@ -51,6 +51,23 @@ class GCN2:
         self.w2 = ((torch.rand((hidden, out_dim), generator=g, device=dev) * 2 - 1) / math.sqrt(hidden)).contiguous()
         self.zero_b1 = torch.zeros(hidden, device=dev)
         self.lr = lr
+        self.side = None
+
+    def use_side_stream(self, enable=True):
+        """Run the independent dW2 product on a second stream (its own
+        gnna context) so it overlaps the dP1 chain; capturable in a CUDA
+        graph (fork/join through stream waits)."""
+        if not enable:
+            self.side = None
+            return self
+
+        class _Side:
+            pass
+        side = _Side()
+        side.stream = torch.cuda.Stream(device=self.row_ptr.device)
+        side.ctx = Context(self.row_ptr.device.index or 0, side.stream)
+        self.side = side
+        return self
 
     def _agg(self, x, relu=False, mask=None, out=None):
         """Â x for an x nobody pre-scaled: K3 gathers norm[u] per edge."""
@@ -99,7 +116,16 @@ class GCN2:
             dp1 = dh1 * (s["h1"] > 0)
             dp1_scaled = False
         else:
-            dw2 = ctx_gemm_tn(ctx, s["z2"], dy)                    # (Â h1)^T dY
+            # (Â h1)^T dY does not feed the rest of the backward: with a side
+            # context it runs on a second stream, overlapped with the dP1 chain
+            side = self.side
+            if side is not None:
+                main = torch.cuda.current_stream()
+                side.stream.wait_stream(main)
+                with torch.cuda.stream(side.stream):
+                    dw2 = ctx_gemm_tn(side.ctx, s["z2"], dy)
+            else:
+                dw2 = ctx_gemm_tn(ctx, s["z2"], dy)                # (Â h1)^T dY
             dz2 = ctx.gemm(dy, w2t, None, 2, self.norm)            # norm * (dY W2^T)
             # Â^T dZ2 masked by relu'(h1) (the sign of a pre-scaled h1 is the same);
             # pre-scaled by norm again when the next aggregation consumes it
@@ -110,6 +136,8 @@ class GCN2:
             dw1 = ctx_gemm_tn(ctx, x, dt1)                         # x^T dT1
         else:
             dw1 = ctx_gemm_tn(ctx, s["z1"], dp1)
+        if out_dim >= hid and self.side is not None:
+            torch.cuda.current_stream().wait_stream(self.side.stream)  # join before dW2 is read
         return dw1, dw2
 
     def sgd(self, dw1, dw2):
