@@ -73,6 +73,14 @@ gnna_status gnna_set_l2_window(gnna_ctx* ctx, const void* base, uint64_t bytes, 
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
         if (hit_ratio < 0.0 || hit_ratio > 1.0) gnna::raise(GNNA_ERR_DOMAIN, "set_l2_window: hit_ratio in [0, 1]");
+        // the persisting-L2 limit is a property of the current device: make it the context's
+        int prev = 0;
+        GNNA_CUDA(cudaGetDevice(&prev));
+        struct Restore {
+            int d;
+            ~Restore() { cudaSetDevice(d); }
+        } restore{prev};
+        GNNA_CUDA(cudaSetDevice(ctx->device));
         cudaStreamAttrValue v{};
         if (!bytes || !base) {
             v.accessPolicyWindow.num_bytes = 0;
