@@ -509,7 +509,9 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
-    traffic, traffic_src = ncu_traffic(args.workload) if world == 1 else (None, None)
+    # the committed ncu capture is of the default configuration only
+    default_cfg = args.order == "degree" and not args.no_l2_pin and args.agg == "sum" and not (args.ngs or args.dw or args.tpb)
+    traffic, traffic_src = ncu_traffic(args.workload) if (world == 1 and default_cfg) else (None, None)
     extras = None
     if rank == 0 and world == 1 and not args.no_extras and args.workload == "c5":
         try:
@@ -537,7 +539,11 @@ def run_ours(args):
                          "frac": achieved / peak, "frac_of_nominal_8TBps": achieved / 8000.0,
                          "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src, "kernel": "k3_aggregate (+k3b_fixup)", "kernel_ms": t_agg,
-                         "algorithmic_bytes_per_launch": balg_rank},
+                         "algorithmic_bytes_per_launch": balg_rank,
+                         # measured DRAM bytes per launch (ncu) over the live kernel time: the
+                         # hardware view of the same launch (B_alg counts L2 hits as traffic)
+                         "dram_GBps_from_traffic": (traffic / (t_agg * 1e-3) / 1e9) if traffic else None,
+                         "dram_frac_from_traffic": (traffic / (t_agg * 1e-3) / 1e9 / peak) if traffic else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
