@@ -213,23 +213,33 @@ __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32
 }
 
 
-// Occupancy vs. loads-in-flight, measured on B200 (profiles/README.md, r01
-// A/B): register-capped occupancy beats deep unrolling.  Wide teams (d >= 32
-// fp32) run 6 row vectors in flight per lane at <= 64 registers (4 CTAs of
-// 256 threads per SM); narrow teams (d = 16) hold 32/TEAM indices per lane,
-// so they run 8 in flight at <= 80 registers (3 CTAs).  GNNA_K3_UNR /
-// GNNA_K3_MINB override both for experiment builds (`make variants`).
-template <int TEAM, int KMAX>
+// Occupancy vs. loads-in-flight, measured on B200 (profiles/README.md):
+// register-capped occupancy beats deep unrolling.  Every plain gather runs 6
+// row vectors in flight per lane at <= 64 registers (4 CTAs of 256 threads
+// per SM): the r01m small-team A/B on C3 (d = 16) measured UNR/minb 6/4 at
+// 0.0563 ms against 8/3 at 0.0645 ms (4/5: 0.0625, 4/6: 0.079, 8/4: 0.073).
+// The per-source-weight gather (EW) on narrow teams holds one more value per
+// row vector and spills at 64 registers, so it keeps 8 in flight at <= 80
+// registers (3 CTAs): 0.080 vs 0.095 ms.  GNNA_K3_UNR / GNNA_K3_MINB (all
+// teams) and GNNA_K3_UNR_S / GNNA_K3_MINB_S (plain narrow teams) override for
+// experiment builds (`make variants`).
+template <int TEAM, int KMAX, bool EW = false>
 struct K3Tune {
+#ifndef GNNA_K3_UNR_S
+#define GNNA_K3_UNR_S 6
+#endif
+#ifndef GNNA_K3_MINB_S
+#define GNNA_K3_MINB_S 4
+#endif
 #ifdef GNNA_K3_UNR
     static constexpr int unr1 = GNNA_K3_UNR;
 #else
-    static constexpr int unr1 = TEAM >= 8 ? 6 : 8;
+    static constexpr int unr1 = TEAM >= 8 ? 6 : (EW ? 8 : GNNA_K3_UNR_S);
 #endif
 #ifdef GNNA_K3_MINB
     static constexpr int minb = GNNA_K3_MINB;
 #else
-    static constexpr int minb = TEAM >= 8 ? 4 : 3;
+    static constexpr int minb = TEAM >= 8 ? 4 : (EW ? 3 : GNNA_K3_MINB_S);
 #endif
     static constexpr int unr = KMAX == 1 ? unr1 : (KMAX == 2 ? (unr1 + 1) / 2 : (unr1 + 3) / 4);
 #ifdef GNNA_K3_BATCH
@@ -254,8 +264,8 @@ template <class T, int VEC, int TEAM, int KMAX, bool EW = false>
 __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64_t e, uint32_t lane,
                                             const uint32_t (&off)[KMAX], const bool (&ok)[KMAX],
                                             Vec<T, VEC> (&acc)[KMAX]) {
-    constexpr int UNR = K3Tune<TEAM, KMAX>::unr;
-    constexpr int BATCH = K3Tune<TEAM, KMAX>::batch;  // CSR entries per index batch
+    constexpr int UNR = K3Tune<TEAM, KMAX, EW>::unr;
+    constexpr int BATCH = K3Tune<TEAM, KMAX, EW>::batch;  // CSR entries per index batch
     constexpr int R = BATCH / TEAM;                    // indices held per lane per batch
     const T* __restrict__ x = static_cast<const T*>(a.x);
     const uint32_t* __restrict__ col = a.col;
@@ -306,7 +316,7 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
 
 // ----------------------------------------------------------------- K3 ---
 template <class T, int VEC, int TEAM, int KMAX, bool EW, bool FAN = false>
-__global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX>::minb) k3_aggregate(AggArgs a) {
+__global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX, EW>::minb) k3_aggregate(AggArgs a) {
     using VT = Vec<T, VEC>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VT* sm = reinterpret_cast<VT*>(smem_raw);  // [upc][KMAX][TEAM]
