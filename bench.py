@@ -291,7 +291,52 @@ def extra_workloads(ctx, dev, reps=10):
                         "frac_of_nominal_8TBps": balg / t / 1e9 / 8000.0, "l2": "flushed between calls"})
         del plan, x, y, rp, col
     out += update_gemms(ctx, dev, scratch, peak, reps)
+    out.append(train_step(ctx, dev, scratch, reps))
     return out
+
+
+def train_step(ctx, dev, scratch, reps):
+    """BASELINE config C3 as a training step (2-layer GCN 96->16->22, fwd +
+    bwd + SGD, fp32) replayed as a CUDA graph; L2 flushed between steps.
+    `bench.py --workload c3train` is the full measurement."""
+    import torch
+    from paper_2006_06608_b200 import synth
+    from paper_2006_06608_b200.gcn import GCN2
+    cfg = synth.CONFIGS["c3"]
+    _, rp, col = synth.build_graph(cfg, lambda n, e: ctx.to_csr(n, e, True), dev)
+    n, nnz = cfg.n, int(col.numel())
+    model = GCN2(ctx, rp, col, 96, 16, 22, self_loops=False)
+    g = torch.Generator(device=dev)
+    g.manual_seed(6)
+    x = synth.features(n, 96, cfg.seed, dev)
+    dy = (torch.rand((n, 22), generator=g, device=dev) - 0.5).contiguous()
+    for _ in range(3):
+        model.step(x, dy)
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(main)
+    ctx.set_stream(cap)
+    graph = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.graph(graph, stream=cap):
+            model.step(x, dy)
+    finally:
+        ctx.set_stream(main)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        scratch.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        graph.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = float(np.median(ts))
+    return {"workload": cfg.name, "train_step": "2-layer GCN 96->16->22, fwd+bwd+SGD, fp32, CUDA graph",
+            "n": n, "nnz": nnz, "ms_per_step": t, "aggregations": model.aggregations_per_step(),
+            "l2": "flushed between steps"}
 
 
 def update_gemms(ctx, dev, scratch, peak, reps):
