@@ -231,15 +231,21 @@ struct K3Tune {
 #ifndef GNNA_K3_MINB_S
 #define GNNA_K3_MINB_S 4
 #endif
+#ifndef GNNA_K3_UNR_W
+#define GNNA_K3_UNR_W 6
+#endif
+#ifndef GNNA_K3_MINB_W
+#define GNNA_K3_MINB_W 4
+#endif
 #ifdef GNNA_K3_UNR
     static constexpr int unr1 = GNNA_K3_UNR;
 #else
-    static constexpr int unr1 = TEAM >= 8 ? 6 : (EW ? 8 : GNNA_K3_UNR_S);
+    static constexpr int unr1 = TEAM >= 8 ? GNNA_K3_UNR_W : (EW ? 8 : GNNA_K3_UNR_S);
 #endif
 #ifdef GNNA_K3_MINB
     static constexpr int minb = GNNA_K3_MINB;
 #else
-    static constexpr int minb = TEAM >= 8 ? 4 : (EW ? 3 : GNNA_K3_MINB_S);
+    static constexpr int minb = TEAM >= 8 ? GNNA_K3_MINB_W : (EW ? 3 : GNNA_K3_MINB_S);
 #endif
     static constexpr int unr = KMAX == 1 ? unr1 : (KMAX == 2 ? (unr1 + 1) / 2 : (unr1 + 3) / 4);
 #ifdef GNNA_K3_BATCH
