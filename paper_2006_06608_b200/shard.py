@@ -58,6 +58,9 @@ def allgather_rows(y, ranges, rank, group=None):
     return y
 
 
+BARRIER_TIMEOUT_MS = 120_000  # a peer that never arrives fails the run instead of hanging it
+
+
 class FusedRowGather:
     """The per-layer all-gather fused into the aggregation (SURVEY §8(e),
     "fused target").  The output y lives in torch symmetric memory, mapped
@@ -109,7 +112,7 @@ class FusedRowGather:
                 if has and int(h.multicast_ptr):
                     mc = int(h.multicast_ptr) + offset
             y.zero_()
-            h.barrier(channel=0)
+            h.barrier(channel=0, timeout_ms=BARRIER_TIMEOUT_MS)
             return cls(y, h, peers, mc, "multimem" if mc else "p2p")
         except Exception:
             return None
@@ -120,7 +123,7 @@ class FusedRowGather:
             plan.aggregate_fanout(x, self.y, mc=self.mc, **opts)
         else:
             plan.aggregate_fanout(x, self.y, peers=self.peers, **opts)
-        self.handle.barrier(channel=0)
+        self.handle.barrier(channel=0, timeout_ms=BARRIER_TIMEOUT_MS)
         return self.y
 
     def verify(self, plan, x, ranges, rank):
@@ -133,7 +136,7 @@ class FusedRowGather:
         plan.aggregate(x, out=ref)
         allgather_rows(ref, ranges, rank)
         self.y.zero_()
-        self.handle.barrier(channel=0)
+        self.handle.barrier(channel=0, timeout_ms=BARRIER_TIMEOUT_MS)
         self.aggregate(plan, x)
         ok = torch.tensor([1 if torch.equal(self.y, ref) else 0], device=self.y.device)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
