@@ -454,6 +454,10 @@ def run_ours(args):
     fused = None
     if world > 1 and args.agg == "sum" and not args.nccl_gather:
         fused = FusedRowGather.create(tuple(x.shape), x.dtype, dev, multicast=args.multimem)
+        ok = torch.tensor([1 if fused is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if not bool(ok.item()):
+            fused = None
         if fused is not None and not fused.verify(plan, x, ranges, rank):
             fused = None  # a replica disagreed with the NCCL path: keep NCCL
         if fused is not None:
