@@ -285,6 +285,113 @@ __global__ void __launch_bounds__(ROWS) k6_gemm_f32(GemmArgs g) {
     }
 }
 
+// X·W for narrow widths whose rows are not 16-byte multiples (k <= 32,
+// k % 4 != 0, n <= 32: the C3 output layer's 22 columns in dZ = dY·W2^T), so
+// TMA cannot tile A.  A CTA's 128 rows of A are ONE contiguous run of 128·k floats,
+// 16-byte aligned whatever k is, so they are streamed with flat float4 loads
+// and scattered into shared memory at an odd row pitch (conflict-free
+// row-per-thread reads).  The 128·n outputs go back the same way: staged at
+// an odd pitch, stored as one flat float4 run.  FFMA in k order.
+constexpr int FL_ROWS = 128, FL_K = 32, FL_LD = FL_ROWS * FL_K / 4 / FL_ROWS;
+// Persistent: a CTA walks tiles blockIdx.x, +gridDim.x, ... and issues the
+// next tile's A loads before computing the current one (latency overlap).
+template <int NJ>
+__global__ void __launch_bounds__(FL_ROWS) k6_gemm_flat(GemmArgs g) {
+    __shared__ float sa[FL_ROWS * (FL_K + 1)];
+    __shared__ float so[FL_ROWS * (FL_K + 1)];
+    __shared__ __align__(16) float sw[FL_K * NJ];
+    const uint32_t k = g.k, n = g.n, kp = k | 1u, np = n | 1u, t = threadIdx.x;
+    // f / k for f < 128·32 without integer division: (f + 0.5)·(1/k) is at
+    // least 0.5/k >= 1/64 from the next integer, far above the float error.
+    const float rk = 1.f / (float)(k ? k : 1), rn = 1.f / (float)n;
+    auto spos = [](uint32_t f, uint32_t w, float rw, uint32_t pitch) {
+        const uint32_t r = (uint32_t)(((float)f + 0.5f) * rw);
+        return r * pitch + (f - r * w);
+    };
+    const uint64_t tiles = (g.m + FL_ROWS - 1) / FL_ROWS;
+    auto tile_rows = [&](uint64_t tile) {
+        const uint64_t r0 = tile * FL_ROWS;
+        return g.m - r0 < (uint64_t)FL_ROWS ? (uint32_t)(g.m - r0) : (uint32_t)FL_ROWS;
+    };
+    float4 v[FL_LD];
+    auto load = [&](uint64_t tile) {
+        const float4* a4 = reinterpret_cast<const float4*>(static_cast<const float*>(g.a) + tile * FL_ROWS * k);
+        const uint32_t nv = tile_rows(tile) * k / 4;
+#pragma unroll
+        for (int i = 0; i < FL_LD; ++i) {
+            const uint32_t e = t + i * FL_ROWS;
+            if (e < nv) v[i] = __ldg(a4 + e);
+        }
+    };
+    for (uint32_t e = t; e < FL_K * NJ; e += FL_ROWS) {
+        const uint32_t r = e / NJ, c = e % NJ;
+        sw[e] = (r < k && c < n) ? __ldg(static_cast<const float*>(g.w) + (uint64_t)r * n + c) : 0.f;
+    }
+    uint64_t tile = blockIdx.x;
+    if (tile < tiles) load(tile);
+    for (; tile < tiles; tile += gridDim.x) {
+        const uint64_t row0 = tile * FL_ROWS;
+        const uint32_t rows = tile_rows(tile);
+        const float* __restrict__ a = static_cast<const float*>(g.a) + row0 * k;
+        const uint32_t cnt = rows * k, nv = cnt / 4;
+#pragma unroll
+        for (int i = 0; i < FL_LD; ++i) {
+            const uint32_t e = t + i * FL_ROWS;
+            if (e < nv) {
+                const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sa[spos(e * 4 + q, k, rk, kp)] = x[q];
+            }
+        }
+        for (uint32_t f = nv * 4 + t; f < cnt; f += FL_ROWS) sa[spos(f, k, rk, kp)] = a[f];
+        __syncthreads();
+        if (tile + gridDim.x < tiles) load(tile + gridDim.x);
+        if (t < rows) {
+            float acc[NJ];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+            const float* ar = sa + t * kp;
+#pragma unroll 4
+            for (uint32_t kk = 0; kk < k; ++kk) {
+                const float av = ar[kk];
+#pragma unroll
+                for (int j = 0; j < NJ; j += 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(&sw[kk * NJ + j]);
+                    acc[j] = fmaf(av, w4.x, acc[j]);
+                    acc[j + 1] = fmaf(av, w4.y, acc[j + 1]);
+                    acc[j + 2] = fmaf(av, w4.z, acc[j + 2]);
+                    acc[j + 3] = fmaf(av, w4.w, acc[j + 3]);
+                }
+            }
+            const float s = g.epilogue == 2 ? (float)g.row_scale[row0 + t] : 1.f;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                if (j >= (int)n) break;
+                float val = acc[j];
+                if (g.epilogue == 1) {
+                    val += static_cast<const float*>(g.bias)[j];
+                    val = val > 0.f ? val : 0.f;
+                } else if (g.epilogue == 2) {
+                    val *= s;
+                }
+                so[t * np + j] = val;
+            }
+        }
+        __syncthreads();
+        float* __restrict__ o = static_cast<float*>(g.out) + row0 * n;
+        const uint32_t ocnt = rows * n, onv = ocnt / 4;
+        for (uint32_t e = t; e < onv; e += FL_ROWS) {
+            float x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = so[spos(e * 4 + q, n, rn, np)];
+            reinterpret_cast<float4*>(o)[e] = make_float4(x[0], x[1], x[2], x[3]);
+        }
+        for (uint32_t f = onv * 4 + t; f < ocnt; f += FL_ROWS) o[f] = so[spos(f, n, rn, np)];
+        // sa/so are rewritten by the next tile: no thread may still be reading them
+        __syncthreads();
+    }
+}
+
 // X·W, row per thread with DIRECT 16-byte loads of the thread's own A row
 // (no A staging, no barriers in the k loop): a warp instruction reads 16 B of
 // 32 rows, the next instruction the following 16 B (L1 hits), so DRAM sees
@@ -746,6 +853,27 @@ void launch_gemm(gnna_ctx* ctx, const GemmArgs& g, bool exact) {
     if (g.m == 0 || g.n == 0) return;
     if constexpr (std::is_same<T, float>::value) {
         if (!exact) {
+            static const bool no_flat = std::getenv("GNNA_GEMM_NOFLAT") != nullptr;  // A/B switch
+            // Only where the tcgen05 path cannot TMA-tile A (k % 4 != 0): in the
+            // C3 train step the 22 -> 16 product takes 25.1 us here against 41.0
+            // on tcgen05 with scalar A loads, while 16 -> 22 stays on TMA (22.9
+            // us, flat 24.2; ncu, profiles/r01p_gemm_flat.md).
+            if (!no_flat && g.k <= (uint32_t)FL_K && g.n <= (uint32_t)FL_K && g.k % 4 != 0 &&
+                (uintptr_t)g.a % 16 == 0 && (uintptr_t)g.out % 16 == 0) {
+                static const int per_sm = std::getenv("GNNA_FLAT_CTAS") ? std::atoi(std::getenv("GNNA_FLAT_CTAS")) : 4;
+                const uint64_t tiles = (g.m + FL_ROWS - 1) / FL_ROWS;
+                const dim3 grid((unsigned)std::min<uint64_t>(tiles, (uint64_t)per_sm * ctx->num_sms));
+                if (g.n <= 8)
+                    k6_gemm_flat<8><<<grid, FL_ROWS, 0, ctx->stream>>>(g);
+                else if (g.n <= 16)
+                    k6_gemm_flat<16><<<grid, FL_ROWS, 0, ctx->stream>>>(g);
+                else if (g.n <= 24)
+                    k6_gemm_flat<24><<<grid, FL_ROWS, 0, ctx->stream>>>(g);
+                else
+                    k6_gemm_flat<32><<<grid, FL_ROWS, 0, ctx->stream>>>(g);
+                gnna::launched(ctx, "k6_gemm_flat");
+                return;
+            }
             static const bool simt = std::getenv("GNNA_GEMM_SIMT") != nullptr;  // A/B switch
             if (!simt && gnna::gemm_tc_f32(ctx, static_cast<const float*>(g.a), static_cast<const float*>(g.w),
                                            static_cast<const float*>(g.bias), g.row_scale, static_cast<float*>(g.out),

@@ -97,3 +97,30 @@ def test_gemm_tn_tc(ctx, m, p, q):
     bound = np.abs(a64).T @ np.abs(b64)
     err = np.abs(got - want)
     assert (err <= 1e-5 * bound + 1e-30).all(), float((err / bound).max())
+
+
+@pytest.mark.parametrize("m,k,n", [(410236, 22, 16), (410236, 22, 22), (3001, 22, 16), (3001, 30, 32), (131, 5, 7),
+                                   (257, 1, 3), (64, 31, 9)])
+def test_gemm_flat_narrow_epilogues(ctx, m, k, n):
+    """k <= 32 with k % 4 != 0, n <= 32 (the C3 output layer's 22 columns):
+    k6_gemm_flat, FFMA over flat float4 row runs, persistent over tiles.  Plain, bias+ReLU and row-scale epilogues, ragged
+    last CTA, and a 4-byte-offset A (falls back to the tcgen05 scalar path)."""
+    rng = np.random.default_rng(m + 31 * k + n)
+    a = ((rng.random((m, k)) - 0.3) * np.exp2(rng.integers(-8, 8, (m, k)))).astype(np.float32)
+    w = (rng.random((k, n)) - 0.5).astype(np.float32)
+    b = (rng.random(n) - 0.5).astype(np.float32)
+    s = rng.random(m)
+    da, dw, db, ds = to_dev(a, w, b, s)
+    a64, w64, b64 = a.astype(np.float64), w.astype(np.float64), b.astype(np.float64)
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        got = ctx.gemm(da, dw)
+        torch.cuda.synchronize()
+    assert any("k6_gemm_flat" in e.name for e in prof.events())
+    check(got.cpu().numpy(), a64, w64)
+    check(ctx.gemm(da, dw, db, 1).cpu().numpy(), a64, w64,
+          lambda y, bd: (np.maximum(0.0, y + b64), bd + np.abs(b64)))
+    check(ctx.gemm(da, dw, None, 2, ds).cpu().numpy(), a64, w64,
+          lambda y, bd: (s[:, None] * y, s[:, None] * bd))
+    flat = torch.zeros(m * k + 1, dtype=torch.float32, device="cuda")
+    flat[1:] = da.reshape(-1)
+    check(ctx.gemm(flat[1:].view(m, k), dw).cpu().numpy(), a64, w64)
