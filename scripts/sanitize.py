@@ -1,6 +1,8 @@
 """Small GPU workload exercising every kernel family once, for compute-sanitizer
 (memcheck / racecheck / synccheck).  Exits non-zero on any parity error."""
 import os
+
+os.environ.setdefault("GNNA_FLAT_CTAS", "1")  # k6_gemm_flat persistent loop with few CTAs
 import sys
 
 import numpy as np
@@ -60,7 +62,8 @@ def main():
     ctx.apply_mapping_csr(drp, dcol, o2n, n2o)
     m = GCN2(ctx, drp, dcol, 24, 16, 8)
     m.step(dev(x).float(), dev(rng.random((n, 8))).float())
-    # tcgen05 GEMMs: TMA-fed (k % 4 == 0), register-fed (k = 22), both dW kernels, fused epilogues
+    # tcgen05 GEMMs: TMA-fed (k % 4 == 0), both dW kernels, fused epilogues;
+    # k = 22 runs k6_gemm_flat (persistent loop: GNNA_FLAT_CTAS=1 below, 157 tiles on 148 CTAs)
     from paper_2006_06608_b200.gcn import ctx_gemm_tn
     for k, q in ((96, 16), (22, 16), (16, 22), (64, 64)):
         a = dev(rng.random((n, k)) - 0.5).float()
@@ -71,6 +74,9 @@ def main():
         ctx.gemm(a, wq, dev(rng.random(q)).float(), 1)
         ctx.gemm(a, wq, None, 2, dev(rng.random(n)))
         assert torch.allclose(ctx_gemm_tn(ctx, a, g).double(), a.double().t() @ g.double(), rtol=1e-4, atol=1e-3)
+    a = dev(rng.random((20000, 22)) - 0.5).float()
+    wq = dev(rng.random((22, 16)) - 0.5).float()
+    assert torch.allclose(ctx.gemm(a, wq).double(), a.double() @ wq.double(), rtol=1e-4, atol=1e-4)
     # fused all-gather: K3 fan-out into local replicas
     p = Params.make(ngs=16, dw=16, tpb=256, dim=32)
     plan = ctx.plan(drp, dcol, p, 2, rows=(100, 2500))
