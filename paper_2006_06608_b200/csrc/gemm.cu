@@ -958,9 +958,15 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
                                                (int)sbytes));
             k6_gemm_tn_small<TI, TJ><<<ctas, 256, sbytes, ctx->stream>>>(a, b, m, p, q, rpc, part.get());
             gnna::launched(ctx, "k6_gemm_tn_small");
-            k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
-                part.get(), ctas, total, out);
-            gnna::launched(ctx, "k6_reduce_chunks_warp");
+            static const bool seq = std::getenv("GNNA_TN_SEQ_REDUCE") != nullptr;  // A/B switch
+            if (seq) {
+                k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
+                    part.get(), ctas, total, out);
+                gnna::launched(ctx, "k6_reduce_chunks_warp");
+            } else {
+                gnna::k_reduce_partials<<<(total + 31) / 32, 1024, 0, ctx->stream>>>(part.get(), ctas, total, out);
+                gnna::launched(ctx, "k_reduce_partials");
+            }
             return;
         }
         if (p <= 128 && q <= 32) {
@@ -991,9 +997,15 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
             }
 #undef GNNA_TNW
             gnna::launched(ctx, "k6_gemm_tn_warp");
-            k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
-                part.get(), ctas, total, out);
-            gnna::launched(ctx, "k6_reduce_chunks_warp");
+            static const bool seq = std::getenv("GNNA_TN_SEQ_REDUCE") != nullptr;  // A/B switch
+            if (seq) {
+                k6_reduce_chunks_warp<<<gnna::grid_for((uint64_t)total * 32, 256), 256, 0, ctx->stream>>>(
+                    part.get(), ctas, total, out);
+                gnna::launched(ctx, "k6_reduce_chunks_warp");
+            } else {
+                gnna::k_reduce_partials<<<(total + 31) / 32, 1024, 0, ctx->stream>>>(part.get(), ctas, total, out);
+                gnna::launched(ctx, "k_reduce_partials");
+            }
             return;
         }
         const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)out % 16 == 0);

@@ -662,7 +662,8 @@ void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
 //     the two column halves.
 // M = 128 reads 4 A slices from the stage base: the 4 - PS phantom slices
 // alias the following bytes (in bounds) and only feed discarded rows of D.
-// Per-CTA partials are summed in CTA order by k6_tn_reduce (deterministic).
+// Per-CTA partials are summed by k_reduce_partials in a fixed slice order
+// (deterministic; GNNA_TN_SEQ_REDUCE=1 keeps the sequential CTA-order k6_tn_reduce).
 // ---------------------------------------------------------------------------
 constexpr int TN_BK = 64;
 
@@ -907,8 +908,14 @@ bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uin
     TnArgs g{m, p, q, nblk, bpc, part.get()};
     kern<<<ctas, TN_THREADS, C::SMEM, ctx->stream>>>(amap, bmap, g);
     launched(ctx, "k6_gemm_tn_tc");
-    k6_tn_reduce<<<(total + 255) / 256, 256, 0, ctx->stream>>>(part.get(), ctas, total, out);
-    launched(ctx, "k6_tn_reduce");
+    static const bool seq = std::getenv("GNNA_TN_SEQ_REDUCE") != nullptr;  // A/B switch
+    if (seq) {
+        k6_tn_reduce<<<(total + 255) / 256, 256, 0, ctx->stream>>>(part.get(), ctas, total, out);
+        launched(ctx, "k6_tn_reduce");
+    } else {
+        k_reduce_partials<<<(total + 31) / 32, 1024, 0, ctx->stream>>>(part.get(), ctas, total, out);
+        launched(ctx, "k_reduce_partials");
+    }
     return true;
 }
 

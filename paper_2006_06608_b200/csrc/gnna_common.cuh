@@ -112,6 +112,32 @@ uint64_t reduce_sum_u64(gnna_ctx* ctx, const uint64_t* d_in, uint64_t count);
 void sort_pairs_u64_u32(gnna_ctx* ctx, uint64_t* keys, uint32_t* vals, uint64_t count, int end_bit);
 void sort_keys_u64(gnna_ctx* ctx, uint64_t* keys, uint64_t count, int end_bit);
 
+// Deterministic sum of per-CTA partials part[chunks][total] -> out[total]
+// (the split-row dW products).  A block covers 32 outputs x 32 chunk slices:
+// loads are coalesced across outputs, each slice sums chunks s, s+32, ... in
+// order, and slice 0 adds the 32 slice sums in slice order.  Fixed order for
+// a given (chunks, total), with ~chunks/32 loads per thread in flight.
+template <int SLICES = 32>
+__global__ void __launch_bounds__(32 * SLICES) k_reduce_partials(const float* __restrict__ part, uint32_t chunks,
+                                                                 uint32_t total, float* __restrict__ out) {
+    __shared__ float red[SLICES][33];
+    const uint32_t tx = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const uint32_t o = blockIdx.x * 32 + tx;
+    float s = 0.f;
+    if (o < total) {
+#pragma unroll 4
+        for (uint32_t c = sl; c < chunks; c += SLICES) s += part[(size_t)c * total + o];
+    }
+    red[sl][tx] = s;
+    __syncthreads();
+    if (sl == 0 && o < total) {
+        float t = 0.f;
+#pragma unroll
+        for (int i = 0; i < SLICES; ++i) t += red[i][tx];
+        out[o] = t;
+    }
+}
+
 }  // namespace gnna
 
 // Internal plan (gnna_plan is opaque at the ABI).
