@@ -948,7 +948,9 @@ void launch_gemm_tn(gnna_ctx* ctx, const T* a, const T* b, uint32_t m, uint32_t 
         const size_t sbytes = std::max<size_t>((size_t)2 * TS_BK * (p + q), (size_t)(256 / std::max(tiles, 1u)) * p * q) * 4;
         static const bool no_small = std::getenv("GNNA_TN_WARP") != nullptr;  // A/B switch
         if (!no_small && tiles <= 256 && sbytes <= 96 * 1024) {
-            uint32_t ctas = std::max<uint32_t>(1, std::min<uint32_t>(4 * ctx->num_sms, (m + TS_BK - 1) / TS_BK));
+            static const uint32_t per_sm =
+                std::getenv("GNNA_TN_SMALL_CTAS") ? (uint32_t)std::atoi(std::getenv("GNNA_TN_SMALL_CTAS")) : 4u;
+            uint32_t ctas = std::max<uint32_t>(1, std::min<uint32_t>(per_sm * ctx->num_sms, (m + TS_BK - 1) / TS_BK));
             const uint32_t rpc = ((m + ctas - 1) / ctas + TS_BK - 1) / TS_BK * TS_BK;
             ctas = (m + rpc - 1) / rpc;
             const uint32_t total = p * q;
