@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
     const uint32_t t = threadIdx.x, grp = t / tiles, tile = t % tiles;
     const bool active = grp < rg;
     const uint32_t ti = (tile / tq) * TI, tj = (tile % tq) * TJ;
+    // vector shared reads of the staged rows (stage bases are 16-byte aligned:
+    // sb starts 2·TS_BK·p floats in, each buffer is TS_BK rows long)
+    const bool va4 = p % 4 == 0, vb2 = q % 2 == 0;
     const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_cta;
     const uint64_t r_end = r_begin + rows_per_cta < m ? r_begin + rows_per_cta : m;
     const uint32_t nblk = r_end > r_begin ? (uint32_t)((r_end - r_begin + TS_BK - 1) / TS_BK) : 0u;
@@ -758,10 +761,24 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
 #pragma unroll 4
             for (uint32_t k = grp; k < nr; k += rg) {
                 float av[TI], bv[TJ];
+                if (TI == 4 && va4) {  // p % 4 == 0: one 16-byte shared load
+                    const float4 x4 = *reinterpret_cast<const float4*>(xa + k * p + ti);
+                    av[0] = x4.x, av[1] = x4.y, av[2] = x4.z, av[3] = x4.w;
+                } else {
 #pragma unroll
-                for (int i = 0; i < TI; ++i) av[i] = ti + i < p ? xa[k * p + ti + i] : 0.f;
+                    for (int i = 0; i < TI; ++i) av[i] = ti + i < p ? xa[k * p + ti + i] : 0.f;
+                }
+                if (TJ % 2 == 0 && vb2) {  // q even: 8-byte shared loads, pairs wholly in or out
 #pragma unroll
-                for (int j = 0; j < TJ; ++j) bv[j] = tj + j < q ? xb[k * q + tj + j] : 0.f;
+                    for (int j = 0; j < TJ; j += 2) {
+                        const float2 y2 = tj + j < q ? *reinterpret_cast<const float2*>(xb + k * q + tj + j)
+                                                     : make_float2(0.f, 0.f);
+                        bv[j] = y2.x, bv[j + 1] = y2.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < TJ; ++j) bv[j] = tj + j < q ? xb[k * q + tj + j] : 0.f;
+                }
 #pragma unroll
                 for (int i = 0; i < TI; ++i)
 #pragma unroll
