@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the C3/C4 north-star side measurements")
     ap.add_argument("--cpu-nodes", type=int, default=0, help="CPU-baseline sample size (nodes)")
     ap.add_argument("--flush-l2", action="store_true", help="force an L2 flush between steps")
-    ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gin"],
-                    help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized), gin (sum + (1+eps)x)")
+    ap.add_argument("--agg", default="sum", choices=["sum", "gcn", "gcn_layer", "gin"],
+                    help="aggregation flavour: sum (aggregate_scheduled), gcn (normalized, gathered norm[u]), "
+                         "gcn_layer (GCN layer form, source scale pre-applied), gin (sum + (1+eps)x)")
     ap.add_argument("--no-l2-pin", action="store_true", help="do not pin the hub rows of x in L2")
     ap.add_argument("--side-stream", action="store_true",
                     help="c3train: dW2 on a second stream (measured slower: 0.464 vs 0.440 ms, kernels contend)")
@@ -63,6 +64,9 @@ def parse():
                     help="N > 1: fused gather through the NVLS multicast address (multimem.st) instead of P2P stores")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N > 1: keep the NCCL broadcast-per-owner all-gather instead of the fused K3 fan-out")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-run ncu traffic probe")
+    ap.add_argument("--probe", default="", choices=["", "main", "extras"], help=argparse.SUPPRESS)
+    ap.add_argument("--probe-out", default="", help=argparse.SUPPRESS)
     ap.add_argument("--evaluator", default="b200", choices=["b200", "reference"],
                     help="parameter choice: B200 cost model (default) or the reference's decider rules")
     return ap.parse_args()
@@ -129,14 +133,95 @@ class Clocks:
                 "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())}
 
 
-def ncu_traffic(workload):
-    """DRAM bytes per launch of K3 from the committed ncu --set full capture
-    (profiles/ncu_traffic.json), or None."""
+NCU_METRICS = ("gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,"
+               "lts__t_sector_hit_rate.pct,dram__throughput.avg.pct_of_peak_sustained_elapsed,"
+               "lts__throughput.avg.pct_of_peak_sustained_elapsed")
+
+
+def ncu_path():
+    for p in (os.environ.get("NCU"), "/usr/local/cuda/bin/ncu", "ncu"):
+        if p and (os.path.sep not in p or os.path.exists(p)):
+            return p
+    return None
+
+
+def parse_ncu_raw(path):
+    """Rows (dict metric -> float, plus 'Kernel Name') of an `ncu --page raw
+    --csv --print-units base` log: header line, units line, one line per
+    profiled launch."""
+    import csv
+    lines = open(path, errors="replace").read().splitlines()
+    start = next((i for i, l in enumerate(lines) if l.startswith('"ID"')), None)
+    if start is None:
+        return []
+    rows = list(csv.reader(lines[start:]))
+    head = rows[0]
+    out = []
+    for r in rows[2:]:
+        if len(r) != len(head):
+            continue
+        d = {"Kernel Name": r[head.index("Kernel Name")]}
+        for h, v in zip(head, r):
+            try:
+                d[h] = float(v.replace(",", ""))
+            except ValueError:
+                pass
+        out.append(d)
+    return out
+
+
+def ncu_probe(args, mode, cache_control, timeout=600):
+    """DRAM / L2 traffic of the timed kernels, measured in THIS bench run: a
+    child process rebuilds the same workload (`--probe <mode>`) and runs it
+    under `ncu --metrics` (one replayed launch per kernel, kernels selected by
+    the NVTX range "probe"), after warm-up calls outside the range.  Returns
+    (list of per-launch metric dicts, the child's per-call launch groups, note)."""
+    ncu = ncu_path()
+    if ncu is None:
+        return None, None, "ncu not found"
+    fd, log = tempfile.mkstemp(suffix=".csv")
+    os.close(fd)
+    fd, groups = tempfile.mkstemp(suffix=".json")
+    os.close(fd)
+    cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "--cache-control", cache_control,
+           "--nvtx", "--nvtx-include", "probe/", "--page", "raw", "--csv", "--print-units", "base",
+           "--log-file", log, sys.executable, os.path.abspath(__file__), "--probe", mode, "--probe-out", groups,
+           "--workload", args.workload, "--agg", args.agg, "--order", args.order, "--evaluator", args.evaluator]
+    for k in ("ngs", "dw", "tpb"):
+        if getattr(args, k):
+            cmd += [f"--{k}", str(getattr(args, k))]
+    if args.no_l2_pin:
+        cmd.append("--no-l2-pin")
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[workload]
-        return d["dram_bytes_per_launch"], d["source"]
-    except Exception:
-        return None, None
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        rows = parse_ncu_raw(log)
+        grp = json.load(open(groups)) if os.path.getsize(groups) else None
+        note = f"ncu rc={r.returncode}" + ("" if rows else ": " + (r.stderr or r.stdout)[-300:].replace("\n", " "))
+        return rows, grp, note
+    except Exception as exc:  # reported, not required
+        return None, None, f"ncu probe failed: {exc}"
+    finally:
+        for p in (log, groups):
+            try:
+                os.unlink(p)
+            except OSError:
+                pass
+
+
+def traffic_summary(rows):
+    """Sum of one call's launches (K3 + K3b): DRAM bytes, L2 bytes, ncu time,
+    and the dominant launch's hit rate / throughput percentages."""
+    if not rows:
+        return None
+    top = max(rows, key=lambda d: d.get("gpu__time_duration.sum", 0.0))
+    return {"dram_bytes": int(sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in rows)),
+            "dram_read_bytes": int(sum(d.get("dram__bytes_read.sum", 0) for d in rows)),
+            "lts_bytes": int(sum(d.get("lts__t_bytes.sum", 0) for d in rows)),
+            "ncu_us": sum(d.get("gpu__time_duration.sum", 0) for d in rows) / 1e3,
+            "l2_hit_pct": top.get("lts__t_sector_hit_rate.pct"),
+            "dram_throughput_pct": top.get("dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "lts_throughput_pct": top.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "kernels": [d["Kernel Name"][:80] for d in rows]}
 
 
 def peaks():
@@ -235,69 +320,262 @@ def run_reference(args):
     }), flush=True)
 
 
-def extra_workloads(ctx, dev, reps=10):
-    """The north-star target configs beside the headline: GCN / GIN / sum
-    aggregation on the amazon0505-shape graph (C3, d 16) and the sum on C4
-    (d 64).  K3 kernel time per call (CUDA events, L2 flushed between calls),
-    B200-evaluator params, against the measured HBM peak."""
+# ------------------------------------------------------------ probe windows
+class ProbeWindow:
+    """Marks ONE call of each measured case with the NVTX range "probe" (the
+    ncu child's capture filter) and records how many libgnna launches each
+    call made, so the parent can split ncu's per-launch rows by case."""
+
+    def __init__(self, ctx, out_path):
+        self.ctx, self.out_path, self.groups = ctx, out_path, []
+
+    def capture(self, name, fn, warm=2):
+        import torch
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        l0 = self.ctx.launches
+        torch.cuda.nvtx.range_push("probe")
+        fn()
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
+        self.groups.append([name, self.ctx.launches - l0])
+
+    def close(self):
+        json.dump(self.groups, open(self.out_path, "w"))
+
+
+def split_rows(rows, groups):
+    """ncu's per-launch rows, in launch order, split by (name, launches) groups."""
+    out, i = {}, 0
+    if not rows or not groups:
+        return out
+    for name, k in groups:
+        out[name] = rows[i:i + k]
+        i += k
+    return out
+
+
+def l2_flush_buffer(dev):
+    import torch
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    return torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
+
+
+def time_calls(call, reps, scratch=None, stream=None):
+    """Median CUDA-event time (ms) of `reps` calls, L2 flushed between calls
+    when `scratch` is given (outside the events)."""
+    import torch
+    for _ in range(3):
+        call()
+    ts = []
+    for _ in range(reps):
+        if scratch is not None:
+            scratch.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        call()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def sparse_adj(rp, col, n, values=None):
+    """fp64 torch CSR adjacency on the GPU: the independent checker of the
+    bench's parity fields (cuSPARSE SpMM in float64)."""
+    import torch
+    v = values if values is not None else torch.ones(col.numel(), dtype=torch.float64, device=col.device)
+    return torch.sparse_csr_tensor(rp, col.long(), v, (n, n))
+
+
+def rel_check(got, want, bound=None, tol=1e-5):
+    """Error-aware parity: max |got - want| / (|want| + bound) over every
+    element; bound = the same op on |inputs| (None: inputs non-negative)."""
+    import torch
+    got = got.double()
+    den = want.abs() + (bound if bound is not None else want.abs())
+    err = (got - want).abs()
+    r = torch.where(err == 0, torch.zeros_like(err), err / den.clamp_min(1e-300))
+    worst = float(r.max()) if r.numel() else 0.0
+    return {"elements": int(r.numel()), "max_rel_err": worst, "tol": tol, "ok": worst <= tol,
+            "rule": "|got-want| <= tol*(|want| + sum|terms|), every element vs an fp64 recompute (torch sparse, GPU)"}
+
+
+def agg_cases(ctx, dev):
+    """The north-star target forms beside the headline, as (name, case) pairs:
+    GCN (layer form and standalone gather), GIN and the plain sum on the
+    amazon0505-shape graph (C3, d 16), the sum on C4 (d 64), and the fp64
+    path (the reference's own precision) on C3 and C4.  Yields after each
+    workload's cases so the graph is freed before the next."""
     import torch
     from paper_2006_06608_b200 import synth
     from paper_2006_06608_b200.capi import WARP_SHARED
-    peak, _ = peaks()
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    scratch = torch.empty(2 * l2 // 4, dtype=torch.float32, device=dev)
-    out = []
-    for w, aggs in (("c3", ("sum", "gcn", "gcn_gather", "gin")), ("c4", ("sum",))):
+    for w, aggs in (("c3", ("sum", "gcn", "gcn_gather", "gin", "sum_f64")), ("c4", ("sum", "sum_f64"))):
         cfg = synth.CONFIGS[w]
         _, rp, col = synth.build_graph(cfg, lambda n, e: ctx.to_csr(n, e, True), dev)
         nnz = int(col.numel())
         x = synth.features(cfg.n, cfg.dim, cfg.seed, dev)
         y = torch.empty_like(x)
+        x64 = x.double()
+        y64 = torch.empty_like(x64)
         p, _ = ctx.b200_params(rp, cfg.dim)
         plan = ctx.plan(rp, col, p, WARP_SHARED)
         rs, sw, _ = ctx.gcn_weights(rp, col, False, edge_weights=False)
         xs = x * rs[:, None]  # the GCN layer's K3 input: norm * (X W) out of the update GEMM's epilogue
+        forms = {
+            "sum": (lambda: plan.aggregate(x, out=y), y, 0, "aggregate_scheduled"),
+            # layer form: y = norm * (A xs [+ self * xs]); no implicit self loops here
+            "gcn": (lambda: plan.aggregate_ex(xs, out=y, row_scale=rs), y, 4 * cfg.n,
+                    "D^-1/2 (A [+I]) D^-1/2 as in the GCN layer: source scale in the update GEMM's epilogue, "
+                    "K3 = plain sum + destination scale + self term"),
+            # standalone form on an arbitrary x: K3 gathers norm[u] per edge
+            "gcn_gather": (lambda: plan.aggregate_ex(x, out=y, node_weight=rs, self_weight=sw, row_scale=rs), y,
+                           4 * nnz + 8 * cfg.n, "D^-1/2 (A [+I]) D^-1/2 x on an arbitrary x: K3 gathers norm[u] per edge"),
+            "gin": (lambda: plan.aggregate_ex(x, out=y, alpha=1.1), y, 4 * cfg.dim * cfg.n, "sum + (1+eps) x"),
+            "sum_f64": (lambda: plan.aggregate(x64, out=y64), y64, None,
+                        "aggregate_scheduled in fp64 (the reference's FeatureMatrix precision; bitwise its tree)"),
+        }
+
+        def reference(agg, _rp=rp, _col=col, _x64=x64, _n=cfg.n):
+            A = sparse_adj(_rp, _col, _n)
+            if agg in ("sum", "sum_f64"):
+                return A @ _x64
+            if agg == "gin":
+                return A @ _x64 + 1.1 * _x64
+            deg = (_rp[1:] - _rp[:-1]).double().clamp_min(1.0)
+            norm = deg.rsqrt()[:, None]
+            return norm * (A @ (norm * _x64))  # normalized_aggregate, no implicit self loops (engine.cpp:338-369)
         for agg in aggs:
-            def call():
-                if agg == "gcn":  # layer form: y = norm * (A xs [+ self * xs]); no implicit self loops here
-                    plan.aggregate_ex(xs, out=y, row_scale=rs)
-                elif agg == "gcn_gather":  # standalone form on an arbitrary x: K3 gathers norm[u] per edge
-                    plan.aggregate_ex(x, out=y, node_weight=rs, self_weight=sw, row_scale=rs)
-                elif agg == "gin":
-                    plan.aggregate_ex(x, out=y, alpha=1.1)
-                else:
-                    plan.aggregate(x, out=y)
-            for _ in range(3):
-                call()
-            ts = []
-            for _ in range(reps):
-                scratch.fill_(1.0)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record()
-                call()
-                b.record()
-                torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            t = float(np.median(ts)) * 1e-3
-            balg = synth.b_alg(cfg.n, nnz, cfg.dim)
-            balg += {"gcn": 4 * cfg.n, "gcn_gather": 12 * cfg.n, "gin": 4 * cfg.dim * cfg.n}.get(agg, 0)
-            form = {"gcn": "D^-1/2 (A [+I]) D^-1/2 as in the GCN layer: source scale in the update GEMM's "
-                           "epilogue, K3 = plain sum + destination scale + self term",
-                    "gcn_gather": "D^-1/2 (A [+I]) D^-1/2 x on an arbitrary x: K3 gathers norm[u] per edge",
-                    "gin": "sum + (1+eps) x", "sum": "aggregate_scheduled"}[agg]
-            out.append({"workload": cfg.name, "aggregation": agg, "form": form, "n": cfg.n, "nnz": nnz, "dim": cfg.dim,
-                        "params": p.tolist()[:3], "kernel_ms": t * 1e3, "edge_dim_per_s": nnz * cfg.dim / t,
-                        "algorithmic_GBps": balg / t / 1e9, "frac_of_measured_hbm": balg / t / 1e9 / peak,
-                        "frac_of_nominal_8TBps": balg / t / 1e9 / 8000.0, "l2": "flushed between calls"})
-        del plan, x, y, rp, col
-    out += update_gemms(ctx, dev, scratch, peak, reps)
+            call, out, extra_b, form = forms[agg]
+            elem = 8 if agg.endswith("f64") else 4
+            balg = synth.b_alg(cfg.n, nnz, cfg.dim, elem) + (extra_b or 0)
+            yield w, cfg, agg, call, out, balg, form, nnz, p, (lambda a=agg: reference(a))
+        del plan, x, y, x64, y64, rp, col, xs
+
+
+def gemm_cases(ctx, dev):
+    """The C3 update GEMMs on tcgen05 (gemm_tc.cu, 3xTF32): X·W (n x 96 · 96
+    x 16, the forward node update) and dW = X^T G (the backward reduction)."""
+    import torch
+    from paper_2006_06608_b200 import synth
+    from paper_2006_06608_b200.gcn import ctx_gemm_tn
+    cfg = synth.CONFIGS["c3"]
+    n, k, q = cfg.n, 96, 16
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    x = torch.rand((n, k), generator=g, device=dev) - 0.5
+    w = torch.rand((k, q), generator=g, device=dev) - 0.5
+    gr = torch.rand((n, q), generator=g, device=dev) - 0.5
+    out = {}
+
+    def xw():
+        out["xw"] = ctx.gemm(x, w)
+
+    def dw():
+        out["dw"] = ctx_gemm_tn(ctx, x, gr)
+
+    def ref_xw():
+        return x.double() @ w.double(), x.double().abs() @ w.double().abs(), out["xw"]
+
+    def ref_dw():
+        return x.double().t() @ gr.double(), x.double().abs().t() @ gr.double().abs(), out["dw"]
+    balg = 4 * n * (k + q) + 4 * k * q
+    yield "xw", "X·W (update, k6_gemm_tc_tma)", [n, k, q], xw, ref_xw, balg
+    yield "dw", "X^T·G (dW, k6_gemm_tn_tc)", [n, k, q], dw, ref_dw, balg
+
+
+def extra_workloads(ctx, dev, args, reps=10):
+    """The north-star target configs beside the headline (C3 / C4 forms, fp64,
+    the C3 update GEMMs, the C3 training step): CUDA-event kernel time per
+    call with L2 flushed between calls, B200-evaluator params, a parity field
+    per line (every element vs an fp64 recompute), and the DRAM / L2 traffic
+    of one call measured by an ncu child of this run."""
+    import torch
+    peak, _ = peaks()
+    scratch = l2_flush_buffer(dev)
+    out = []
+    for w, cfg, agg, call, y, balg, form, nnz, p, reference in agg_cases(ctx, dev):
+        t = time_calls(call, reps, scratch) * 1e-3
+        call()
+        parity = rel_check(y, reference(), tol=1e-12 if agg.endswith("f64") else 1e-5)
+        out.append({"case": f"{w}/{agg}", "workload": cfg.name, "aggregation": agg, "form": form, "n": cfg.n,
+                    "nnz": nnz, "dim": cfg.dim, "dtype": "f64" if agg.endswith("f64") else "f32",
+                    "params": p.tolist()[:3], "kernel_ms": t * 1e3, "edge_dim_per_s": nnz * cfg.dim / t,
+                    "algorithmic_bytes": balg, "effective_GBps": balg / t / 1e9,
+                    "effective_frac_of_measured_hbm": balg / t / 1e9 / peak, "l2": "flushed between calls",
+                    "parity": parity})
+        torch.cuda.empty_cache()
+    for name, label, shape, call, reference, balg in gemm_cases(ctx, dev):
+        t = time_calls(call, reps, scratch) * 1e-3
+        want, bound, got = reference()
+        out.append({"case": f"c3/{name}", "workload": "C3 amazon0505-shape Chung-Lu power law", "gemm": label,
+                    "shape": shape, "dtype": "f32 (3xTF32 on tcgen05)", "kernel_ms": t * 1e3,
+                    "algorithmic_bytes": balg, "effective_GBps": balg / t / 1e9,
+                    "effective_frac_of_measured_hbm": balg / t / 1e9 / peak, "l2": "flushed between calls",
+                    "parity": rel_check(got, want, bound)})
     out.append(train_step(ctx, dev, scratch, reps))
+    # traffic of one call of every case, measured by an ncu child of this run
+    # (cache flushed before each launch, like the timed calls)
+    if not args.no_ncu:
+        rows, groups, note = ncu_probe(args, "extras", "all")
+        per = split_rows(rows, groups)
+        for e in out:
+            tr = traffic_summary(per.get(e.get("case")))
+            if tr is None:
+                e["traffic"] = {"unavailable": note}
+                continue
+            t = e["kernel_ms"] * 1e-3
+            tr["dram_GBps"] = tr["dram_bytes"] / t / 1e9
+            tr["dram_frac_of_measured_hbm"] = tr["dram_GBps"] / peak
+            tr["lts_GBps"] = tr["lts_bytes"] / t / 1e9
+            tr["source"] = "this run: ncu --metrics child (bench.py --probe extras), cache flushed per launch"
+            e["traffic"] = tr
     return out
+
+
+def probe_extras(ctx, dev, args):
+    """Child side of the extras traffic probe: the same cases, one captured call each."""
+    win = ProbeWindow(ctx, args.probe_out)
+    scratch = l2_flush_buffer(dev)
+    for w, cfg, agg, call, *_ in agg_cases(ctx, dev):
+        win.capture(f"{w}/{agg}", call)
+        scratch.fill_(1.0)
+    for name, _, _, call, _, _ in gemm_cases(ctx, dev):
+        win.capture(f"c3/{name}", call)
+    win.close()
+
+
+def gcn2_reference(rp, col, n, x, w1, w2, dy, mask):
+    """fp64 recompute of GCN2's step (y, dW1, dW2) with torch sparse on the GPU:
+    y = Â relu(Â x W1) W2 (each layer ordered as gcn_layer, engine.cpp:373-382),
+    and its gradients; the ReLU-backward uses `mask` (the GPU forward's own, so
+    a pre-activation tied at zero does not flip a whole term).  Returns the
+    values and their sum-of-|terms| bounds."""
+    import torch
+    deg = (rp[1:] - rp[:-1]).double().clamp_min(1.0)
+    nv = deg.rsqrt()
+    vals = nv[torch.repeat_interleave(torch.arange(n, device=rp.device), rp[1:] - rp[:-1])] * nv[col.long()]
+    A = sparse_adj(rp, col, n, vals)
+    x, w1, w2, dy = x.double(), w1.double(), w2.double(), dy.double()
+    pre = A @ (x @ w1)
+    h1 = pre.clamp_min(0)
+    z2 = A @ h1
+    y = z2 @ w2
+    dw2 = z2.t() @ dy
+    dp1 = (A @ (dy @ w2.t())) * mask
+    dw1 = x.t() @ (A @ dp1)
+    ax, aw1, aw2, ady = x.abs(), w1.abs(), w2.abs(), dy.abs()
+    bpre = A @ (ax @ aw1)
+    bz2 = A @ bpre
+    bdp1 = A @ (ady @ aw2.t())
+    return (y, dw1, dw2, pre), (bz2 @ aw2, ax.t() @ (A @ bdp1), bz2.t() @ ady, bpre)
 
 
 def train_step(ctx, dev, scratch, reps):
     """BASELINE config C3 as a training step (2-layer GCN 96->16->22, fwd +
     bwd + SGD, fp32) replayed as a CUDA graph; L2 flushed between steps.
+    One step with lr = 0 is checked first against an fp64 recompute.
     `bench.py --workload c3train` is the full measurement."""
     import torch
     from paper_2006_06608_b200 import synth
@@ -310,6 +588,7 @@ def train_step(ctx, dev, scratch, reps):
     g.manual_seed(6)
     x = synth.features(n, 96, cfg.seed, dev)
     dy = (torch.rand((n, 22), generator=g, device=dev) - 0.5).contiguous()
+    parity = train_parity(model, rp, col, n, x, dy)
     for _ in range(3):
         model.step(x, dy)
     torch.cuda.synchronize()
@@ -324,85 +603,71 @@ def train_step(ctx, dev, scratch, reps):
     finally:
         ctx.set_stream(main)
     torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
-        scratch.fill_(1.0)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        graph.replay()
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    t = float(np.median(ts))
-    return {"workload": cfg.name, "train_step": "2-layer GCN 96->16->22, fwd+bwd+SGD, fp32, CUDA graph",
+    t = time_calls(graph.replay, reps, scratch)
+    return {"case": "c3/train_step", "workload": cfg.name,
+            "train_step": "2-layer GCN 96->16->22, fwd+bwd+SGD, fp32, CUDA graph",
             "n": n, "nnz": nnz, "ms_per_step": t, "aggregations": model.aggregations_per_step(),
-            "l2": "flushed between steps"}
+            "l2": "flushed between steps", "parity": parity}
 
 
-def update_gemms(ctx, dev, scratch, peak, reps):
-    """The C3 update GEMMs on tcgen05 (gemm_tc.cu, 3xTF32): X·W1 (n x 96 ·
-    96 x 16, the forward node update) and dW1 = X^T G (the backward
-    reduction).  Kernel time per call (CUDA events, L2 flushed), algorithmic
-    bytes 4·n·(k + n_out) against the measured HBM peak."""
-    import torch
-    from paper_2006_06608_b200 import synth
-    from paper_2006_06608_b200.gcn import ctx_gemm_tn
-    cfg = synth.CONFIGS["c3"]
-    n, k, q = cfg.n, 96, 16
-    g = torch.Generator(device=dev)
-    g.manual_seed(11)
-    x = torch.rand((n, k), generator=g, device=dev) - 0.5
-    w = torch.rand((k, q), generator=g, device=dev) - 0.5
-    gr = torch.rand((n, q), generator=g, device=dev) - 0.5
-    res = []
-    for name, call in (("X·W (update, k6_gemm_tc_tma)", lambda: ctx.gemm(x, w)),
-                       ("X^T·G (dW, k6_gemm_tn_tc)", lambda: ctx_gemm_tn(ctx, x, gr))):
-        for _ in range(3):
-            call()
-        ts = []
-        for _ in range(reps):
-            scratch.fill_(1.0)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            call()
-            b.record()
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        t = float(np.median(ts)) * 1e-3
-        balg = 4 * n * (k + q) + 4 * k * q
-        res.append({"workload": cfg.name, "gemm": name, "shape": [n, k, q], "dtype": "f32 (3xTF32 on tcgen05)",
-                    "kernel_ms": t * 1e3, "algorithmic_GBps": balg / t / 1e9,
-                    "frac_of_measured_hbm": balg / t / 1e9 / peak, "l2": "flushed between calls",
-                    "timing": "one call between events (includes the host-side launch)"})
-    return res
+def train_parity(model, rp, col, n, x, dy):
+    """One lr = 0 step of GCN2 vs gcn2_reference: output, dW1, dW2 at the
+    error-aware 1e-5 bar; ReLU-mask disagreements must be ties."""
+    lr, model.lr = model.lr, 0.0
+    try:
+        y, dw1, dw2 = model.step(x, dy)
+    finally:
+        model.lr = lr
+    mask = (model.saved["h1"] > 0).double()
+    (wy, wdw1, wdw2, pre), (by, bdw1, bdw2, bpre) = gcn2_reference(rp, col, n, x, model.w1, model.w2, dy, mask)
+    flips = (mask > 0) != (pre > 0)
+    ties = bool(((pre.abs() <= 1e-5 * bpre) | ~flips).all())
+    res = {k: rel_check(g, w, b) for k, g, w, b in (("y", y, wy, by), ("dW1", dw1, wdw1, bdw1),
+                                                       ("dW2", dw2, wdw2, bdw2))}
+    return {"ok": all(r["ok"] for r in res.values()) and ties, "relu_mask_flips": int(flips.sum()),
+            "flips_are_ties": ties, **{k: {"max_rel_err": r["max_rel_err"], "ok": r["ok"]} for k, r in res.items()},
+            "tol": 1e-5, "rule": "error-aware 1e-5 vs fp64 torch-sparse recompute of the step (lr = 0)"}
 
 
 # ------------------------------------------------------------------ our arm
-def run_ours(args):
+def headline_forms(ctx, plan, rp, col, x, y, args, n, dim, rows, nnz):
+    """Aggregation flavours on the headline graph's plan: name -> (call,
+    extra algorithmic bytes over B_alg, description).  sum is
+    aggregate_scheduled (engine.cpp:200-311); gcn is normalized_aggregate
+    (engine.cpp:338-369) on an arbitrary x, K3 gathering norm[u] per edge
+    with the self weight and the row scale in its flush; gcn_layer is the
+    GCN layer's form (x pre-scaled by the update GEMM's epilogue, so K3 is a
+    plain sum plus the destination scale); gin is sum + (1 + eps) x."""
+    forms = {"sum": (lambda: plan.aggregate(x, out=y), 0, "aggregate_scheduled (sum)")}
+    if args.agg == "gin" or (args.extras_c5 and args.agg == "sum"):
+        forms["gin"] = (lambda: plan.aggregate_ex(x, out=y, alpha=1.0 + 0.1), 4 * dim * rows,
+                        "GIN sum + (1+eps) x, eps 0.1 (fused)")
+    if args.agg in ("gcn", "gcn_layer") or (args.extras_c5 and args.agg == "sum"):
+        rs, sw, _ = ctx.gcn_weights(rp, col, False, edge_weights=False)
+        forms["gcn"] = (lambda: plan.aggregate_ex(x, out=y, node_weight=rs, self_weight=sw, row_scale=rs),
+                        4 * nnz + 8 * rows, "GCN normalized_aggregate D^-1/2 A D^-1/2 x on an arbitrary x "
+                                           "(K3 gathers norm[u] per edge; self weight and row scale fused)")
+        xs = x * rs[:, None]
+        forms["gcn_layer"] = (lambda: plan.aggregate_ex(xs, out=y, row_scale=rs), 4 * rows,
+                              "GCN layer form: x pre-scaled by norm in the update GEMM's epilogue, "
+                              "K3 = plain sum + destination scale")
+    return forms
+
+
+def setup_headline(args, ctx, dev, world, rank):
+    """The headline workload on this rank: graph, degree order, features,
+    plan over the rank's row range, hub L2 window."""
     import torch
-    import torch.distributed as dist
     from paper_2006_06608_b200 import synth
-    from paper_2006_06608_b200.capi import WARP_SHARED, Context
-    from paper_2006_06608_b200.shard import FusedRowGather, allgather_rows, row_ranges
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
-    ctx = Context(local, stream)
+    from paper_2006_06608_b200.capi import WARP_SHARED
+    from paper_2006_06608_b200.shard import row_ranges
+    S = {}
     cfg = synth.CONFIGS[args.workload]
-
     t0 = time.time()
     edges, rp, col = synth.build_graph(cfg, lambda n, e: ctx.to_csr(n, e, True), dev)
     del edges
-    n = cfg.n
-    nnz = int(col.numel())
-    x = synth.features(n, cfg.dim, cfg.seed, dev)
-    gen_s = time.time() - t0
+    x = synth.features(cfg.n, cfg.dim, cfg.seed, dev)
+    S["gen_s"] = time.time() - t0
     # preprocessing (untimed, like the reference's renumbering stage): degree
     # order puts the power-law hubs in one contiguous front block of x
     order = {"order": args.order}
@@ -414,12 +679,9 @@ def run_ours(args):
         del o2n, n2o
         torch.cuda.synchronize()
         order["renumber_s"] = round(time.time() - t1, 3)
-    y = torch.zeros_like(x)
     rp_host = rp.cpu().numpy().view(np.uint64)
     ranges = row_ranges(rp_host, world)
     r0, r1 = ranges[rank]
-    my_nnz = int(rp_host[r1] - rp_host[r0])
-
     # Parameters: the performance evaluator with the B200 profile, unless overridden.
     if args.evaluator == "reference":
         p = ctx.auto_params(ctx.model_inputs(rp, cfg.dim, b200=True))  # decider.cpp rules
@@ -434,46 +696,78 @@ def run_ours(args):
     t1 = time.time()
     plan = ctx.plan(rp, col, p, WARP_SHARED, rows=(r0, r1))
     torch.cuda.synchronize()
-    plan_s = time.time() - t1
-
+    S["plan_s"] = time.time() - t1
     # L2 residency for the hub rows (gnna_set_l2_window), only when the front
     # rows carry a disproportionate share of the gathers
-    l2_pin = ctx.pin_hot_rows(rp_host, x) if not args.no_l2_pin else {"pinned": False, "disabled": True}
+    S["l2_pin"] = ctx.pin_hot_rows(rp_host, x) if not args.no_l2_pin else {"pinned": False, "disabled": True}
+    S.update(cfg=cfg, rp=rp, col=col, x=x, y=torch.zeros_like(x), rp_host=rp_host, ranges=ranges, r0=r0, r1=r1,
+             p=p, plan=plan, order=order, nnz=int(col.numel()), my_nnz=int(rp_host[r1] - rp_host[r0]))
+    S["forms"] = headline_forms(ctx, plan, rp, col, x, S["y"], args, cfg.n, cfg.dim, r1 - r0, S["my_nnz"])
+    return S
+
+
+def probe_main(ctx, dev, args):
+    """Child side of the headline traffic probe: one captured call per form,
+    after warm-up calls (the L2 window is set as in the timed region)."""
+    S = setup_headline(args, ctx, dev, 1, 0)
+    win = ProbeWindow(ctx, args.probe_out)
+    for name, (call, _, _) in S["forms"].items():
+        win.capture(name, call)
+    win.close()
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2006_06608_b200 import synth
+    from paper_2006_06608_b200.capi import Context
+    from paper_2006_06608_b200.shard import FusedRowGather, allgather_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(local, stream)
+    if args.probe:
+        (probe_main if args.probe == "main" else probe_extras)(ctx, dev, args)
+        return
+    args.extras_c5 = world == 1 and not args.no_extras and args.workload == "c5"
+    S = setup_headline(args, ctx, dev, world, rank)
+    cfg, rp, col, x, y, plan, p = S["cfg"], S["rp"], S["col"], S["x"], S["y"], S["plan"], S["p"]
+    r0, r1, ranges, rp_host, n, nnz = S["r0"], S["r1"], S["ranges"], S["rp_host"], cfg.n, S["nnz"]
+    l2_pin = S["l2_pin"]
 
     x_bytes = x.numel() * 4
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = args.flush_l2 or x_bytes < 4 * l2
     scratch = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device=dev) if flush else None
 
-    # --agg: sum = aggregate_scheduled; gcn = normalized_aggregate (engine.cpp:338-369)
-    # fused into K3 (per-edge norm[col], self weight, row scale); gin = sum + (1+eps) x
-    gw = ctx.gcn_weights(rp, col, False, edge_weights=False) if args.agg == "gcn" else None
-
     # multi-GPU: the all-gather fused into K3 through symmetric memory (NVLS
     # multicast or P2P stores), else one NCCL broadcast per owner
-    fused = None
+    fused, fused_note = None, None
     if world > 1 and args.agg == "sum" and not args.nccl_gather:
-        fused = FusedRowGather.create(tuple(x.shape), x.dtype, dev, multicast=args.multimem)
+        fused, fused_note = FusedRowGather.create(tuple(x.shape), x.dtype, dev, multicast=args.multimem)
         ok = torch.tensor([1 if fused is not None else 0], device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
         if not bool(ok.item()):
-            fused = None
+            fused, fused_note = None, fused_note or "another rank could not set up symmetric memory"
         if fused is not None and not fused.verify(plan, x, ranges, rank):
-            fused = None  # a replica disagreed with the NCCL path: keep NCCL
+            fused, fused_note = None, "verify: a fused replica differed from the NCCL path"
         if fused is not None:
             y = fused.y
     gather_mode = "single GPU" if world == 1 else (f"fused into K3 ({fused.mode})" if fused else
-                                                     "NCCL broadcast per owner (allgather_rows)")
+                                                     f"NCCL broadcast per owner (allgather_rows): {fused_note}")
+    headline_call, extra_bytes, agg_desc = S["forms"][args.agg]
 
     def agg():
         if fused is not None:
             fused.aggregate(plan, x)
-        elif args.agg == "gcn":
-            plan.aggregate_ex(x, out=y, node_weight=gw[0], self_weight=gw[1], row_scale=gw[0])
-        elif args.agg == "gin":
-            plan.aggregate_ex(x, out=y, alpha=1.0 + 0.1)
         else:
-            plan.aggregate(x, out=y)
+            headline_call()
 
     def step():
         agg()
@@ -509,12 +803,10 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
     launches = ctx.launches - launches0
-    if l2_pin.get("pinned"):
-        ctx.set_l2_window(None, 0)  # the e2e and side measurements run on other buffers
     step_ms = [a.elapsed_time(c) for a, _, c in ev]
     agg_ms = [a.elapsed_time(b) for a, b, _ in ev]
-    t_step = sum(step_ms) / len(step_ms)
-    t_agg = sum(agg_ms) / len(agg_ms)
+    t_step = float(np.median(step_ms))  # median of the timed runs
+    t_agg = float(np.median(agg_ms))
     if world > 1:
         tt = torch.tensor([t_step, t_agg], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -522,16 +814,42 @@ def run_ours(args):
     clocks = clk.summary()
 
     value = nnz * cfg.dim / (t_step * 1e-3)
-    balg_rank = synth.b_alg(r1 - r0, my_nnz, cfg.dim)
-    if args.agg == "gcn":  # + per-edge weights, row scale and self weight per row
-        balg_rank += 8 * (r1 - r0) + 4 * n  # norm (row scale + gathered node weight) and self weights
-    elif args.agg == "gin":  # + the self row x[v]
-        balg_rank += 4 * cfg.dim * (r1 - r0)
+    balg_rank = synth.b_alg(r1 - r0, S["my_nnz"], cfg.dim) + extra_bytes
     peak, peak_src = peaks()
-    achieved = balg_rank / (t_agg * 1e-3) / 1e9
+    effective = balg_rank / (t_agg * 1e-3) / 1e9
 
-    # correctness spot check of this run against the CPU oracle on sampled rows
+    # correctness spot check of this run on sampled rows (fp64 recompute)
     check = spot_check(rp_host, col, x, y, ranges if world > 1 else [(r0, r1)], cfg.dim, agg=args.agg)
+
+    # the C5 GCN / GIN forms on the same graph and plan (one GPU)
+    c5_extras = []
+    if args.extras_c5:
+        for name, (call, xb, desc) in S["forms"].items():
+            if name == args.agg:
+                continue
+            t = time_calls(call, max(5, min(args.steps, 10)), None, stream) * 1e-3
+            bb = synth.b_alg(r1 - r0, S["my_nnz"], cfg.dim) + xb
+            c5_extras.append({"case": f"c5/{name}", "workload": cfg.name, "aggregation": name, "form": desc,
+                              "n": n, "nnz": nnz, "dim": cfg.dim, "dtype": "f32", "kernel_ms": t * 1e3,
+                              "edge_dim_per_s": nnz * cfg.dim / t, "algorithmic_bytes": bb,
+                              "effective_GBps": bb / t / 1e9, "effective_frac_of_measured_hbm": bb / t / 1e9 / peak,
+                              "l2": "inputs > L2; hub L2 window as the headline",
+                              "parity": spot_check(rp_host, col, x, y, [(r0, r1)], cfg.dim, agg=name)})
+    if l2_pin.get("pinned"):
+        ctx.set_l2_window(None, 0)  # the e2e and side measurements run on other buffers
+
+    # DRAM / L2 traffic of the timed kernels, measured by an ncu child of THIS run
+    traffic = {"unavailable": "N > 1 (ncu profiles one process)" if world > 1 else "--no-ncu"}
+    if rank == 0 and world == 1 and not args.no_ncu:
+        rows, groups, note = ncu_probe(args, "main", "none")
+        per = split_rows(rows, groups)
+        traffic = traffic_summary(per.get(args.agg)) or {"unavailable": note}
+        for e in c5_extras:
+            tr = traffic_summary(per.get(e["aggregation"]))
+            if tr:
+                tr["dram_frac_of_measured_hbm"] = tr["dram_bytes"] / (e["kernel_ms"] * 1e-3) / 1e9 / peak
+            e["traffic"] = tr or {"unavailable": note}
+    dram = traffic.get("dram_bytes") if isinstance(traffic, dict) else None
 
     # ---------------- e2e through the host-buffer C-ABI entry (pinned buffers)
     e2e = None
@@ -558,16 +876,17 @@ def run_ours(args):
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {exc}"}
 
-    # the committed ncu capture is of the default configuration only
-    default_cfg = args.order == "degree" and not args.no_l2_pin and args.agg == "sum" and not (args.ngs or args.dw or args.tpb)
-    traffic, traffic_src = ncu_traffic(args.workload) if (world == 1 and default_cfg) else (None, None)
     extras = None
-    if rank == 0 and world == 1 and not args.no_extras and args.workload == "c5":
+    if args.extras_c5:
         try:
-            extras = extra_workloads(ctx, dev)
+            extras = c5_extras + extra_workloads(ctx, dev, args)
         except Exception as exc:  # reported, not required
-            extras = [{"error": str(exc)}]
+            extras = c5_extras + [{"error": repr(exc)}]
     if rank == 0:
+        if dram:
+            achieved, traffic_src = dram / (t_agg * 1e-3) / 1e9, "this run: ncu --metrics child (bench.py --probe main)"
+        else:
+            achieved, traffic_src = effective, None
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
@@ -575,24 +894,25 @@ def run_ours(args):
             "config": {"workload": cfg.name, "n": n, "nnz": nnz, "dim": cfg.dim,
                        "params": {"ngs": p.ngs, "dw": p.dw, "tpb": p.tpb, "tpw": p.tpw},
                        "strategy": "WarpShared", "dim_mode": "Cyclic", "parallelism": f"rows{world}",
-                       "allgather": gather_mode,
+                       "allgather": gather_mode, "timing": "median of the timed steps (CUDA events)",
                        "ms_aggregate_vs_gather": [round(t_agg, 4), round(t_step - t_agg, 4)],
-                       "aggregation": {"sum": "aggregate_scheduled (sum)",
-                                       "gcn": "GCN normalized_aggregate D^-1/2 A D^-1/2 x (fused)",
-                                       "gin": "GIN sum + (1+eps) x, eps 0.1 (fused)"}[args.agg],
+                       "aggregation": agg_desc,
                        "l2": "flushed between steps" if flush else f"inputs ({x_bytes / 1e9:.2f} GB x) > L2 ({l2 / 1e6:.0f} MB)",
-                       "l2_window": l2_pin, "node_order": order,
-                       "plan": plan.info(), "graph_build_s": round(gen_s, 3), "plan_build_s": round(plan_s, 3),
+                       "l2_window": l2_pin, "node_order": S["order"],
+                       "plan": plan.info(), "graph_build_s": round(S["gen_s"], 3),
+                       "plan_build_s": round(S["plan_s"], 3),
                        "max_degree": int(np.diff(rp_host).max())},
+            # achieved / frac: DRAM bytes of the timed kernels (ncu, this run) over
+            # their CUDA-event time: the hardware's view.  effective_*: the SURVEY
+            # §8(d) algorithmic bytes (B_alg counts L2 hits as traffic) over the same time.
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "frac_of_nominal_8TBps": achieved / 8000.0,
-                         "traffic": traffic, "traffic_source": traffic_src,
+                         "traffic": dram, "traffic_source": traffic_src, "traffic_detail": traffic,
+                         "achieved_basis": "dram_bytes (ncu, this run)" if dram else "algorithmic bytes (no ncu)",
                          "peak_source": peak_src, "kernel": "k3_aggregate (+k3b_fixup)", "kernel_ms": t_agg,
-                         "algorithmic_bytes_per_launch": balg_rank,
-                         # measured DRAM bytes per launch (ncu) over the live kernel time: the
-                         # hardware view of the same launch (B_alg counts L2 hits as traffic)
-                         "dram_GBps_from_traffic": (traffic / (t_agg * 1e-3) / 1e9) if traffic else None,
-                         "dram_frac_from_traffic": (traffic / (t_agg * 1e-3) / 1e9 / peak) if traffic else None},
+                         "algorithmic_bytes_per_launch": balg_rank, "effective_GBps": effective,
+                         "effective_frac": effective / peak,
+                         "l2_hit_pct": traffic.get("l2_hit_pct") if isinstance(traffic, dict) else None},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -624,7 +944,7 @@ def spot_check(rp_host, col, x, y, ranges, dim, rows=2000, agg="sum"):
         for k, v in enumerate(pick):
             nb = col_h[rp_host[v]:rp_host[v + 1]]
             xs = x[torch_index(nb, x.device)].cpu().numpy().astype(np.float64) if len(nb) else np.zeros((0, dim))
-            if agg == "gcn":
+            if agg in ("gcn", "gcn_layer"):  # no implicit self loops: the self weight is 0
                 want = norm[v] * (norm[nb][:, None] * xs).sum(0)
             else:
                 want = xs.sum(0)

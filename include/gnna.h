@@ -129,7 +129,12 @@ GNNA_API gnna_status gnna_build_mem_plan(gnna_ctx* ctx, const uint32_t* d_part2n
  * rebuilds this inside every aggregate_scheduled call (engine.cpp:213-221);
  * here it is built once and reused.  The plan keeps pointers to d_row_ptr and
  * d_col, which must outlive it.  Strategy NaiveAtomic/UnitSync flush every
- * unit on its own, WarpShared per Algorithm-1 run. */
+ * unit on its own, WarpShared per Algorithm-1 run.
+ * Streams: the plan's arrays are allocated (stream-ordered) on the context's
+ * stream at creation and freed on that stream by gnna_plan_destroy, so that
+ * stream must outlive the plan.  A plan holds mutable carry scratch: do not
+ * run aggregations of ONE plan on two streams concurrently (one plan per
+ * stream; plans over the same CSR are cheap). */
 GNNA_API gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col,
                              uint32_t n, uint32_t row_begin, uint32_t row_end,
                              const gnna_params* p, int strategy, gnna_plan** out);

@@ -110,6 +110,24 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def _dev(t, what, dtype=None, shape=None):
+    """Argument check before a device pointer crosses the C-ABI: a contiguous
+    CUDA tensor of the expected dtype / shape (the kernels take raw row-major
+    pointers and sizes, so a view or a width mismatch would read or write out
+    of bounds instead of failing)."""
+    if t is None:
+        return t
+    if not getattr(t, "is_cuda", False):
+        raise ValueError(f"{what}: expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: expected a contiguous tensor (got strides {tuple(t.stride())})")
+    if dtype is not None and t.dtype not in (dtype if isinstance(dtype, tuple) else (dtype,)):
+        raise TypeError(f"{what}: expected dtype {dtype}, got {t.dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{what}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
 def _dtype_code(t):
     import torch
     if t.dtype == torch.float32:
@@ -343,6 +361,11 @@ class Context:
         n_out = w.shape[1]
         if out is None:
             out = self.torch.empty((m, n_out), dtype=a.dtype, device=a.device)
+        _dev(a, "a", (self.torch.float32, self.torch.float64))
+        _dev(w, "w", a.dtype, (k, n_out))
+        _dev(out, "out", a.dtype, (m, n_out))
+        _dev(bias, "bias", a.dtype, (n_out,))
+        _dev(row_scale, "row_scale", self.torch.float64, (m,))  # gnna_gemm takes a double row scale
         self._check(self.L.gnna_gemm(self.h, C.c_int(_dtype_code(a)), _ptr(a), C.c_uint32(m), C.c_uint32(k), _ptr(w),
                                      C.c_uint32(n_out), _ptr(bias), C.c_int(epilogue), _ptr(row_scale), _ptr(out)))
         return out
@@ -541,9 +564,17 @@ class Plan:
         self.ctx._check(self.ctx.L.gnna_plan_info(self.h, C.byref(g), C.byref(r), C.byref(s), C.byref(c)))
         return {"groups": g.value, "runs": r.value, "split_nodes": s.value, "carries": c.value}
 
+    def _feat(self, x, out, width=None):
+        torch = self.ctx.torch
+        width = x.shape[1] if width is None else width
+        _dev(x, "x", (torch.float32, torch.float64), (self.n, width))
+        _dev(out, "out", x.dtype, (self.n, width))
+
     def aggregate(self, x, out=None, dim_mode=DIM_CYCLIC):
         if out is None:
             out = self.ctx.torch.zeros_like(x)
+        # gnna_aggregate uses the plan's dim: x must have exactly that width
+        self._feat(x, out, self.params.dim)
         self.ctx._check(self.ctx.L.gnna_aggregate(self.ctx.h, self.h, C.c_int(_dtype_code(x)),
                                                   C.c_int(dim_mode), _ptr(x), _ptr(out)))
         return out
@@ -553,6 +584,11 @@ class Plan:
         """gnna_aggregate_ex: y = relu?(row_scale * (A (node_weight x) + self_weight * x)) [masked]; any width."""
         if out is None:
             out = self.ctx.torch.empty_like(x)
+        self._feat(x, out)
+        f32 = self.ctx.torch.float32
+        for t, nm in ((node_weight, "node_weight"), (self_weight, "self_weight"), (row_scale, "row_scale")):
+            _dev(t, nm, f32, (self.n,))
+        _dev(mask, "mask", x.dtype, tuple(x.shape))
         o = AggOpts(int(x.shape[1]), _ptr(node_weight), _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu),
                     _ptr(mask))
         self.ctx._check(self.ctx.L.gnna_aggregate_ex(self.ctx.h, self.h, C.c_int(_dtype_code(x)), C.c_int(dim_mode),
@@ -565,6 +601,11 @@ class Plan:
         row also written into each peer replica (device pointers or tensors:
         the other ranks' y, P2P-mapped) or, with `mc`, only through the NVLS
         multicast address of the replicated y."""
+        self._feat(x, out)
+        f32 = self.ctx.torch.float32
+        for t, nm in ((self_weight, "self_weight"), (row_scale, "row_scale")):
+            _dev(t, nm, f32, (self.n,))
+        _dev(mask, "mask", x.dtype, tuple(x.shape))
         peers = [p if isinstance(p, int) else p.data_ptr() for p in peers]
         if len(peers) > 7:
             raise ValueError("at most 7 peer replicas (GNNA_MAX_PEERS)")

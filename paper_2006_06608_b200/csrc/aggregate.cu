@@ -492,10 +492,13 @@ struct Shape {
     uint32_t team, kpl, kmax;
 };
 
-Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const void* x, const void* y) {
+Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const void* x, const void* y,
+                   bool others_aligned = true) {
     Shape s;
     const int full = 16 / elem;
-    const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0);
+    // every row-vector operand (x, y, and the mask / peer replicas / multicast
+    // address when present) must be 16-byte aligned for the vector path
+    const bool aligned = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && others_aligned;
     s.vec = (dim % full == 0 && aligned) ? full : 1;
     const uint32_t nvec = dim / s.vec;
     // The physical lane map is free: every output dimension is summed in the
@@ -607,10 +610,16 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
     if (o && o->node_weight && dtype != GNNA_F32)
         raise(GNNA_ERR_DOMAIN, "aggregate: node weights are supported on the F32 path only");
     const uint32_t wpb = plan->wpb;
-    const Shape s = choose_shape(elem, dim, plan->params.dw, pow2floor(256 / wpb), x, y);
+    bool others = !(o && o->mask) || (uintptr_t)o->mask % 16 == 0;
+    for (uint32_t i = 0; i < npeer && peers; ++i) others = others && (uintptr_t)peers[i] % 16 == 0;
+    others = others && (uintptr_t)mc % 16 == 0;
+    const Shape s = choose_shape(elem, dim, plan->params.dw, pow2floor(256 / wpb), x, y, others);
     // carry slots are sized for the widest dim seen on this plan
     const uint64_t need = plan->ncarry * (uint64_t)dim * 8;
-    if (need > plan->carry.n) plan->carry = DevBuf<uint8_t>(need, ctx->stream);
+    if (need > plan->carry.n) {  // grow on the caller's stream, the old slots freed after their last use
+        plan->carry.release_on(ctx->stream);
+        plan->carry = DevBuf<uint8_t>(need, ctx->stream);
+    }
     AggArgs a{};
     a.part_ptr = plan->part_ptr.get();
     a.part2node = plan->part2node.get();

@@ -83,8 +83,29 @@ struct DevBuf {
         return *this;
     }
     ~DevBuf() { reset(); }
+    // Frees on the allocation stream: that stream must outlive the buffer.
     void reset() {
         if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    // Frees ordered after the work queued so far on BOTH the allocation
+    // stream and `cur` (the stream the buffer was last used on), so a buffer
+    // that moved to another stream (gnna_set_stream) is not released under
+    // work still queued there.  Not for use while `cur` is capturing.
+    void release_on(cudaStream_t cur) {
+        if (!p) return;
+        if (cur != s) {
+            cudaEvent_t e = nullptr;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(e, s);
+                cudaStreamWaitEvent(cur, e, 0);
+                cudaEventDestroy(e);
+            }
+            cudaFreeAsync(p, cur);
+        } else {
+            cudaFreeAsync(p, s);
+        }
         p = nullptr;
         n = 0;
     }

@@ -8,6 +8,8 @@ all-gather is over uneven row blocks, issued as one broadcast per owner.
 """
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 
@@ -91,19 +93,21 @@ class FusedRowGather:
 
     @classmethod
     def create(cls, shape, dtype, device, group=None, multicast=False):
+        """(FusedRowGather, None), or (None, why) when the fused path cannot be
+        set up here; the caller then keeps the NCCL path and reports `why`."""
+        import torch.distributed as dist
+        if not dist.is_initialized() or dist.get_world_size(group) < 2:
+            return None, "needs an initialised process group of at least 2 ranks"
+        if dist.get_world_size(group) - 1 > 7:  # GNNA_MAX_PEERS
+            return None, "more than 8 ranks (GNNA_MAX_PEERS = 7 peer replicas)"
         try:
-            import torch.distributed as dist
             import torch.distributed._symmetric_memory as symm
-            if not dist.is_initialized() or dist.get_world_size(group) < 2:
-                return None
-            if dist.get_world_size(group) - 1 > 7:  # GNNA_MAX_PEERS
-                return None
             y = symm.empty(*shape, dtype=dtype, device=device)
             h = symm.rendezvous(y, group if group is not None else dist.group.WORLD)
             ptrs = list(h.buffer_ptrs)
             offset = y.data_ptr() - int(ptrs[h.rank])
             if offset < 0:
-                return None
+                return None, "symmetric buffer offset is negative"
             peers = cls.peer_pointers(ptrs, h.rank, offset)
             mc = None
             if multicast:
@@ -113,12 +117,20 @@ class FusedRowGather:
                     mc = int(h.multicast_ptr) + offset
             y.zero_()
             h.barrier(channel=0, timeout_ms=BARRIER_TIMEOUT_MS)
-            return cls(y, h, peers, mc, "multimem" if mc else "p2p")
-        except Exception:
-            return None
+            return cls(y, h, peers, mc, "multimem" if mc else "p2p"), None
+        except Exception as exc:  # reported by the caller (config.allgather), never silent
+            warnings.warn(f"FusedRowGather: symmetric memory unavailable, keeping NCCL: {exc!r}")
+            return None, f"symmetric memory unavailable: {exc!r}"[:300]
 
     def aggregate(self, plan, x, **opts):
-        """This rank's rows into every replica, then the cross-rank barrier."""
+        """This rank's rows into every replica, then the cross-rank barrier.
+
+        The barrier BEFORE the fan-out orders this step's remote stores after
+        every rank finished reading the previous step's y (a rank that is
+        ahead must not overwrite rows a slower peer still reads, e.g. when y
+        feeds the next layer); the barrier AFTER orders every rank's reads
+        after all ranks' stores."""
+        self.handle.barrier(channel=0, timeout_ms=BARRIER_TIMEOUT_MS)
         if self.mc:
             plan.aggregate_fanout(x, self.y, mc=self.mc, **opts)
         else:

@@ -245,3 +245,24 @@ def test_l2_window_keeps_results(ctx, orc):
     assert torch.equal(plan.aggregate(x), want)
     # x smaller than L2: the data-driven pin leaves L2 alone
     assert ctx.pin_hot_rows(rp, x)["pinned"] is False
+
+
+def test_capi_argument_checks(ctx, orc):
+    """The ctypes layer refuses what the raw-pointer C-ABI cannot see: views,
+    width mismatches against the plan, wrong dtypes."""
+    from paper_2006_06608_b200.capi import Params
+    rng = np.random.default_rng(1)
+    rp, col, _ = random_graph(rng, 300, 1200, orc=orc)
+    drp, dcol = to_dev(rp, col)
+    plan = ctx.plan(drp, dcol, Params.make(ngs=8, dw=16, tpb=128, dim=16), 2)
+    x = torch.rand((300, 32), device="cuda")
+    with pytest.raises(ValueError):
+        plan.aggregate(x)  # plan dim 16, x width 32
+    with pytest.raises(ValueError):
+        plan.aggregate(x[:, :16])  # a strided view
+    with pytest.raises(TypeError):
+        plan.aggregate(torch.zeros((300, 16), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        plan.aggregate_ex(x, row_scale=torch.ones(299, device="cuda"))
+    y = plan.aggregate_ex(x)  # aggregate_ex takes any width
+    assert y.shape == x.shape

@@ -264,4 +264,5 @@ def test_fused_row_gather_host_logic():
     assert FusedRowGather.peer_pointers([10, 20, 30, 40], 2) == [10, 20, 40]
     assert FusedRowGather.peer_pointers([5], 0) == []
     assert FusedRowGather.peer_pointers([100, 200], 1, offset=8) == [108]
-    assert FusedRowGather.create((4, 4), torch.float32, "cpu") is None
+    fused, why = FusedRowGather.create((4, 4), torch.float32, "cpu")
+    assert fused is None and "process group" in why  # the reason is reported, not swallowed

@@ -95,9 +95,15 @@ def test_gcn_backward(ctx, orc, sl):
         gdx, gdw = ctx.gcn_backward(drp, dcol, dx_, dw_, ddy, sl)
         np.testing.assert_allclose(gdx.cpu().numpy(), wdx, rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(gdw.cpu().numpy(), wdw, rtol=1e-10, atol=1e-12)
+        # fp32 inputs rounded first, so the bar measures the kernels' error only
+        x32, w32, dy32 = (a.astype(np.float32).astype(np.float64) for a in (x, w, dy))
+        wdx, wdw = orc.gcn_backward(rp, col, x32, w32, dy32, sl)
+        bdx, bdw = orc.gcn_backward(rp, col, np.abs(x32), np.abs(w32), np.abs(dy32), sl)
         fdx, fdw = ctx.gcn_backward(drp, dcol, dx_.float(), dw_.float(), ddy.float(), sl)
-        np.testing.assert_allclose(fdx.cpu().numpy(), wdx, rtol=1e-4, atol=1e-5)
-        np.testing.assert_allclose(fdw.cpu().numpy(), wdw, rtol=1e-4, atol=1e-4)
+        ok, r = close32(fdx.cpu().numpy(), wdx, bdx)
+        assert ok, (t, "dx", r)
+        ok, r = close32(fdw.cpu().numpy(), wdw, bdw)
+        assert ok, (t, "dw", r)
 
 
 def test_gin_backward_vs_oracle_and_autograd(ctx, orc):
@@ -118,6 +124,15 @@ def test_gin_backward_vs_oracle_and_autograd(ctx, orc):
         np.testing.assert_allclose(gdw.cpu().numpy(), wdw, rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(gdb.cpu().numpy(), wdb, rtol=1e-10, atol=1e-12)
         assert gde == pytest.approx(wde, rel=1e-10, abs=1e-12)
+        # fp32 within the error-aware 1e-5 bar (bound: the same backward on |inputs|, every ReLU open)
+        x32, w32, b32, dy32 = (a.astype(np.float32).astype(np.float64) for a in (x, w, b, dy))
+        wdx, wdw, wdb, _ = orc.gin_backward(rp, col, x32, eps, w32, b32, dy32)
+        bdx, bdw, bdb, _ = orc.gin_backward(rp, col, np.abs(x32), eps, np.abs(w32), np.abs(b32) + 1.0,
+                                            np.abs(dy32))
+        fdx, fdw, fdb, _ = ctx.gin_backward(drp, dcol, dxx.float(), eps, dww.float(), dbb.float(), ddy.float())
+        for got, want, bnd, nm in ((fdx, wdx, bdx, "dx"), (fdw, wdw, bdw, "dw"), (fdb, wdb, bdb, "db")):
+            ok, r = close32(got.cpu().numpy(), want, bnd)
+            assert ok, (t, nm, r)
         # independent: torch float64 autograd over a dense adjacency
         A = torch.zeros((n, n), dtype=torch.float64)
         for v in range(n):

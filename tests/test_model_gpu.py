@@ -108,11 +108,36 @@ def test_torch_autograd_layers(ctx, orc, dtype):
     H = torch.relu(An @ X @ W1)
     Y = torch.relu((A @ H + 1.2 * H) @ W2 + B2)
     Y.backward(g.double().cpu())
-    tol = dict(rtol=1e-9, atol=1e-11) if dtype == torch.float64 else dict(rtol=1e-3, atol=1e-4)
-    np.testing.assert_allclose(y.detach().double().cpu().numpy(), Y.detach().numpy(), **tol)
-    for got, ref in ((x.grad, X.grad), (l1.weight.grad, W1.grad), (l2.weight.grad, W2.grad), (l2.bias.grad, B2.grad)):
-        r = ref.numpy()
-        np.testing.assert_allclose(got.double().cpu().numpy(), r, rtol=tol["rtol"], atol=tol["atol"] * max(1, np.abs(r).max()))
+    if dtype == torch.float64:
+        tol = dict(rtol=1e-9, atol=1e-11)
+        np.testing.assert_allclose(y.detach().double().cpu().numpy(), Y.detach().numpy(), **tol)
+        for got, ref in ((x.grad, X.grad), (l1.weight.grad, W1.grad), (l2.weight.grad, W2.grad),
+                         (l2.bias.grad, B2.grad)):
+            r = ref.numpy()
+            np.testing.assert_allclose(got.double().cpu().numpy(), r, rtol=tol["rtol"],
+                                       atol=tol["atol"] * max(1, np.abs(r).max()))
+        return
+    # fp32: error-aware 1e-5 bar; the bound is the same network on |inputs| with
+    # every ReLU open (sum of |terms|), its gradients by float64 autograd as well
+    Xb = X.detach().abs().requires_grad_(True)
+    W1b, W2b, B2b = (t.detach().abs().requires_grad_(True) for t in (W1, W2, B2))
+    Hb = An.abs() @ Xb @ W1b
+    Yb = (A @ Hb + 1.2 * Hb) @ W2b + B2b
+    Yb.backward(g.double().cpu().abs())
+    assert_close_bound(y.detach(), Y.detach(), Yb.detach(), "y")
+    for got, ref, bnd, nm in ((x.grad, X.grad, Xb.grad, "dx"), (l1.weight.grad, W1.grad, W1b.grad, "dW1"),
+                              (l2.weight.grad, W2.grad, W2b.grad, "dW2"), (l2.bias.grad, B2.grad, B2b.grad, "db2")):
+        assert_close_bound(got, ref, bnd, nm)
+
+
+def assert_close_bound(got, want, bound, what, rtol=1e-5):
+    """|got - want| <= rtol * (|want| + bound), bound = sum of |terms|."""
+    got = got.double().cpu().numpy() if torch.is_tensor(got) else np.asarray(got, np.float64)
+    want = want.double().cpu().numpy() if torch.is_tensor(want) else np.asarray(want, np.float64)
+    bound = bound.double().cpu().numpy() if torch.is_tensor(bound) else np.asarray(bound, np.float64)
+    err = np.abs(got - want)
+    lim = rtol * (np.abs(want) + bound) + 1e-30
+    assert (err <= lim).all(), (what, float((err / lim).max()))
 
 
 def dense_norm_adj(rp, col, self_loops):
@@ -144,20 +169,24 @@ def test_gcn2_step_vs_autograd_and_reference(ctx, orc, dims, sl):
     w1, w2 = model.w1.double().cpu().numpy(), model.w2.double().cpu().numpy()
     y, dw1, dw2 = model.step(to_dev(x), to_dev(dy))
     # reference semantics: gcn_layer (oracle, fp64) twice with a ReLU between
-    h1 = np.maximum(orc.gcn_layer(rp, col, x.astype(np.float64), w1, sl), 0)
+    x64 = x.astype(np.float64)
+    h1 = np.maximum(orc.gcn_layer(rp, col, x64, w1, sl), 0)
     want = orc.gcn_layer(rp, col, h1, w2, sl)
-    scale = np.abs(want).max()
-    np.testing.assert_allclose(y.cpu().numpy(), want, rtol=1e-4, atol=1e-5 * scale)
-    # gradients: torch float64 autograd
+    bh1 = orc.gcn_layer(rp, col, np.abs(x64), np.abs(w1), sl)
+    assert_close_bound(y, want, orc.gcn_layer(rp, col, bh1, np.abs(w2), sl), "y")
+    # gradients: torch float64 autograd; bound: the same on |inputs|, ReLU open
     An = torch.tensor(dense_norm_adj(rp, col, sl))
     W1 = torch.tensor(w1, requires_grad=True)
     W2 = torch.tensor(w2, requires_grad=True)
     X = torch.tensor(x, dtype=torch.float64)
     Y = An @ torch.relu(An @ X @ W1) @ W2
     Y.backward(torch.tensor(dy, dtype=torch.float64))
-    for got, ref in ((dw1, W1.grad), (dw2, W2.grad)):
-        r = ref.numpy()
-        np.testing.assert_allclose(got.double().cpu().numpy(), r, rtol=1e-3, atol=1e-4 * np.abs(r).max())
+    W1b = W1.detach().abs().requires_grad_(True)
+    W2b = W2.detach().abs().requires_grad_(True)
+    Yb = An @ (An @ X.abs() @ W1b) @ W2b
+    Yb.backward(torch.tensor(np.abs(dy), dtype=torch.float64))
+    for got, ref, bnd, nm in ((dw1, W1.grad, W1b.grad, "dW1"), (dw2, W2.grad, W2b.grad, "dW2")):
+        assert_close_bound(got, ref, bnd, nm)
 
 
 def test_gcn2_step_cuda_graph_replay(ctx, orc):
