@@ -7,6 +7,7 @@ reference's summation tree; fp32 within 1e-5 relative of the fp64 reference
 (inputs are non-negative U[0,1), so no cancellation: SURVEY Appendix A)."""
 import numpy as np
 import pytest
+import torch
 
 from conftest import random_graph, to_dev
 
