@@ -384,9 +384,13 @@ def time_calls(call, reps, scratch=None, stream=None):
 def sparse_adj(rp, col, n, values=None):
     """fp64 torch CSR adjacency on the GPU: the independent checker of the
     bench's parity fields (cuSPARSE SpMM in float64)."""
+    import warnings
+
     import torch
     v = values if values is not None else torch.ones(col.numel(), dtype=torch.float64, device=col.device)
-    return torch.sparse_csr_tensor(rp, col.long(), v, (n, n))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # "sparse CSR support is in beta" / invariant-check notices
+        return torch.sparse_csr_tensor(rp, col.long(), v, (n, n))
 
 
 def rel_check(got, want, bound=None, tol=1e-5):
@@ -732,10 +736,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     ctx = Context(local, stream)
+    args.extras_c5 = world == 1 and not args.no_extras and args.workload == "c5"
     if args.probe:
         (probe_main if args.probe == "main" else probe_extras)(ctx, dev, args)
         return
-    args.extras_c5 = world == 1 and not args.no_extras and args.workload == "c5"
     S = setup_headline(args, ctx, dev, world, rank)
     cfg, rp, col, x, y, plan, p = S["cfg"], S["rp"], S["col"], S["x"], S["y"], S["plan"], S["p"]
     r0, r1, ranges, rp_host, n, nnz = S["r0"], S["r1"], S["ranges"], S["rp_host"], cfg.n, S["nnz"]

@@ -276,11 +276,16 @@ gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
             const uint64_t G = unit_starts(ctx, d_row_ptr, row_begin, rows, p->ngs, us);
             if (G >= (1ull << 32)) gnna::raise(GNNA_ERR_DOMAIN, "plan: more than 2^32 workload units");
             plan->G = G;
-            plan->part_ptr = DevBuf<uint64_t>(G + 1, s);
-            plan->part2node = DevBuf<uint32_t>(G ? G : 1, s);
+            plan->part_ptr = DevBuf<uint64_t>(G + 1 + kPlanPad, s);
+            plan->part2node = DevBuf<uint32_t>(G + kPlanPad, s);
             plan->slot = DevBuf<uint8_t>(G ? G : 1, s);
             plan->leader = DevBuf<uint8_t>(G ? G : 1, s);
-            plan->uflags = DevBuf<uint8_t>(G ? G : 1, s);
+            plan->uflags = DevBuf<uint8_t>(G + kPlanPad, s);
+            plan->tile_counter = DevBuf<uint32_t>(1, s);
+            // the slack is never read as data, but keep it defined (sanitizer initcheck)
+            GNNA_CUDA(cudaMemsetAsync(plan->part_ptr.get() + G + 1, 0, kPlanPad * 8, s));
+            GNNA_CUDA(cudaMemsetAsync(plan->part2node.get() + G, 0, kPlanPad * 4, s));
+            GNNA_CUDA(cudaMemsetAsync(plan->uflags.get() + G, 0, kPlanPad, s));
             plan->cidx = DevBuf<uint32_t>(G ? G : 1, s);
             if (rows) {
                 k1_write<<<gnna::grid_for((uint64_t)rows * 32, 256), 256, 0, s>>>(
