@@ -1,4 +1,4 @@
-// K3 / K3b / K4: neighbor aggregation for sm_100a.
+// K3 / K3A / K4: neighbor aggregation for sm_100a.
 //
 // K3 (scheduled, engine.cpp:200-311): a team of TEAM lanes owns one workload
 // unit (neighbor group).  Lanes split the row into 16-byte vectors (float4 /
@@ -10,7 +10,8 @@
 //   - otherwise partials go to shared memory and the run's leader team sums
 //     them in unit order (= the reference's slot accumulation) and flushes;
 //   - a run of a node spanning several blocks is written to a carry slot and
-//     K3b adds the node's carries in block order.
+//     the last CTA to write one of the node's carries adds them in block
+//     order (carry_arrive); zero-degree rows are written by trailing blocks.
 // The summation tree is the reference's: per unit, sequential over CSR
 // order from 0; per run, sequential over units from 0; per node, sequential
 // over blocks from 0.  In fp64 this makes the result bitwise equal to
@@ -142,6 +143,15 @@ struct AggArgs {
     // look-ahead: CTA k prefetches into L2 the unit metadata of CTA k + pf
     // (the CTA that takes its slot when it retires); 0 = off
     uint32_t pf;
+    // fused carry combine / empty rows (formerly the K3b pass)
+    const uint32_t* carry_split;  // carry slot -> split-node index
+    uint32_t* split_cnt;          // per split node: carries written so far this launch (reset by the last)
+    const uint32_t* split_node;   // per split node: node id
+    const uint32_t* split_first;  // per split node: first carry slot
+    const uint32_t* split_count;  // per split node: carry slots
+    const uint32_t* empty_rows;   // zero-degree rows of the range
+    uint64_t nempty;
+    uint64_t unit_blocks;         // CTAs that own units; blocks past them write empty rows
     // K4 exact modes
     const double* norm;
     const uint8_t* self;
@@ -320,10 +330,63 @@ __device__ __forceinline__ void gather_team(const AggArgs& a, uint64_t b, uint64
     }
 }
 
+// A split node's carries (its runs' partials, one per schedule block it
+// spans) are combined by whichever CTA writes the LAST of them: each writer
+// fences and counts; the last one sums the node's carries in block order
+// (= the reference's flush order, engine.cpp:294-308) and applies the final
+// store.  Deterministic whatever the arrival order, and no second pass.
+template <class T, int VEC, int TEAM, bool FAN>
+__device__ __forceinline__ void carry_arrive(const AggArgs& a, uint32_t c, uint32_t lane) {
+    const uint32_t wl = threadIdx.x & 31;
+    const uint32_t tmask = (TEAM == 32 ? 0xffffffffu : ((1u << TEAM) - 1u)) << (wl - lane);
+    __threadfence();  // this lane's carry stores, before the count
+    __syncwarp(tmask);
+    uint32_t last = 0, k = 0;
+    if (lane == 0) {
+        k = __ldg(a.carry_split + c);
+        last = atomicAdd(a.split_cnt + k, 1u) + 1u == __ldg(a.split_count + k) ? 1u : 0u;
+    }
+    last = __shfl_sync(tmask, last, 0, TEAM);
+    if (!last) return;
+    k = __shfl_sync(tmask, k, 0, TEAM);
+    __threadfence();  // every other writer's carries are visible (they fenced before counting)
+    const uint32_t first = __ldg(a.split_first + k), cnt = __ldg(a.split_count + k), v = __ldg(a.split_node + k);
+    const T* cy = static_cast<const T*>(a.carry) + (size_t)first * a.dim;
+    for (uint32_t ch = lane; ch < a.nvec; ch += TEAM) {
+        Vec<T, VEC> acc;
+        vzero(acc);
+        for (uint32_t j = 0; j < cnt; ++j) {
+            const T* p = cy + (size_t)j * a.dim + ch * VEC;
+            Vec<T, VEC> t;
+#pragma unroll
+            for (int i = 0; i < VEC; ++i) t.a[i] = __ldcg(p + i);  // L2: written by other CTAs
+            vadd(acc, t);
+        }
+        store_final<T, VEC, FAN>(a, v, ch * VEC, acc);
+    }
+    if (lane == 0) a.split_cnt[k] = 0;  // ready for the next launch (stream-ordered)
+}
+
+// Blocks past the unit blocks: zero-degree rows get the epilogue of an empty sum.
+template <class T, int VEC, int TEAM, bool FAN>
+__device__ __forceinline__ void empty_rows_block(const AggArgs& a) {
+    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
+    const uint64_t i = (blockIdx.x - a.unit_blocks) * (uint64_t)(blockDim.x / TEAM) + tu;
+    if (i >= a.nempty) return;
+    const uint32_t v = __ldg(a.empty_rows + i);
+    Vec<T, VEC> z;
+    vzero(z);
+    for (uint32_t ch = lane; ch < a.nvec; ch += TEAM) store_final<T, VEC, FAN>(a, v, ch * VEC, z);
+}
+
 // ----------------------------------------------------------------- K3 ---
 template <class T, int VEC, int TEAM, int KMAX, bool EW, bool FAN = false>
 __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX, EW>::minb) k3_aggregate(AggArgs a) {
     using VT = Vec<T, VEC>;
+    if (blockIdx.x >= a.unit_blocks) {  // block-uniform: no barrier is skipped by part of a CTA
+        empty_rows_block<T, VEC, TEAM, FAN>(a);
+        return;
+    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VT* sm = reinterpret_cast<VT*>(smem_raw);  // [upc][KMAX][TEAM]
     const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
@@ -391,6 +454,7 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX, EW>::minb) k3_aggregat
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k)
                         if (L.ok[k]) stv<T, VEC>(cy + L.off[k], r[k]);
+                    if (k0 + KMAX >= a.kpl) carry_arrive<T, VEC, TEAM, FAN>(a, __ldg(a.cidx + u), lane);
                 } else {
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k)
@@ -402,27 +466,149 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX, EW>::minb) k3_aggregat
     }
 }
 
-// K3b: split nodes add their carried run sums in block order (from 0);
-// empty rows get the epilogue of a zero sum.
-template <class T, int VEC, int TEAM, bool FAN = false>
-__global__ void __launch_bounds__(256) k3b_fixup(AggArgs a, const uint32_t* __restrict__ nodes,
-                                                 const uint32_t* __restrict__ first,
-                                                 const uint32_t* __restrict__ count, uint64_t nsplit,
-                                                 uint64_t nfix) {
-    using VT = Vec<T, VEC>;
-    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
-    const uint64_t i = (uint64_t)blockIdx.x * (256 / TEAM) + tu;
-    if (i >= nfix) return;
-    const uint32_t v = nodes[i];
-    for (uint32_t c = lane; c < a.nvec; c += TEAM) {
-        VT acc;
-        vzero(acc);
-        if (i < nsplit) {
-            const T* cy = static_cast<const T*>(a.carry) + (size_t)first[i] * a.dim + c * VEC;
-            const uint32_t cnt = count[i];
-            for (uint32_t j = 0; j < cnt; ++j) vadd(acc, ldv<T, VEC>(cy + (size_t)j * a.dim));
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---------------------------------------------------------------- K3A ---
+// K3 with the row gather landing in shared memory (cp.async, 16 B per lane
+// per row) instead of registers, for narrow rows (one chunk per lane).  The
+// plain K3 holds its in-flight rows in registers, so memory-level
+// parallelism is capped by the 64-register budget that buys 4 CTAs per SM
+// (6 rows in flight per lane); ncu (r02) shows it latency-bound on exactly
+// those gathers and on the index loads.  Here a lane issues up to K3A_ROWS
+// cp.async row copies into its own smem slots, waits once, then adds the
+// rows in CSR order from shared memory, so the summation tree is unchanged
+// (fp64 bitwise) while rows in flight per lane grow 2-3x at fewer registers
+// (occupancy is now set by shared memory).
+#ifndef K3A_ROWS
+#define K3A_ROWS 12
+#endif
+#ifndef K3A_MINB
+#define K3A_MINB 5
+#endif
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// buf: this warp's slots, row q of lane wl at buf[q * 32 + wl].
+template <class T, int VEC, int TEAM, bool EW>
+__device__ __forceinline__ void gather_async(const AggArgs& a, uint64_t b, uint64_t e, uint32_t lane, uint32_t off,
+                                             bool ok, Vec<T, VEC>& acc, Vec<T, VEC>* buf) {
+    constexpr int ROWS = K3A_ROWS;
+    constexpr int R = 32 / TEAM;  // indices held per lane per 32-entry batch
+    const T* __restrict__ x = static_cast<const T*>(a.x);
+    const uint32_t wl = threadIdx.x & 31;
+    const uint32_t len = (uint32_t)(e - b);
+    const uint32_t wlen = __reduce_max_sync(0xffffffffu, len);
+    for (uint32_t base = 0; base < wlen; base += 32) {
+        uint32_t idxr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t j = base + lane + r * TEAM;
+            idxr[r] = j < len ? __ldg(a.col + b + j) : 0u;
         }
-        store_final<T, VEC, FAN>(a, v, c * VEC, acc);
+        const uint32_t cnt = len > base ? min(32u, len - base) : 0u;
+        const uint32_t wcnt = __reduce_max_sync(0xffffffffu, cnt);
+#pragma unroll
+        for (int q0 = 0; q0 < 32; q0 += ROWS) {  // unrolled: idxr[] indices are compile-time (registers)
+            if ((uint32_t)q0 >= wcnt) break;
+            float wgt[EW ? ROWS : 1];
+#pragma unroll
+            for (int u = 0; u < ROWS; ++u) {
+                const uint32_t q = q0 + u;
+                if (q0 + u < 32) {
+                    uint32_t idx = __shfl_sync(0xffffffffu, idxr[(q0 + u) / TEAM], (q0 + u) % TEAM, TEAM);
+                    if constexpr (EW) wgt[u] = q < cnt ? __ldg(a.nw + idx) : 0.f;
+                    if (ok && q < cnt) cp_async16(smem_addr(&buf[u * 32 + wl]), x + (size_t)idx * a.dim + off);
+                }
+            }
+            cp_async_wait_all();
+#pragma unroll
+            for (int u = 0; u < ROWS; ++u) {
+                if (ok && (uint32_t)(q0 + u) < cnt) {
+                    const Vec<T, VEC> v = buf[u * 32 + wl];
+                    if constexpr (EW) {
+#pragma unroll
+                        for (int i = 0; i < VEC; ++i) acc.a[i] = fmaf(wgt[u], v.a[i], acc.a[i]);
+                    } else {
+                        vadd(acc, v);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <class T, int VEC, int TEAM, bool EW, bool FAN = false>
+__global__ void __launch_bounds__(256, K3A_MINB) k3a_aggregate(AggArgs a) {
+    using VT = Vec<T, VEC>;
+    if (blockIdx.x >= a.unit_blocks) {
+        empty_rows_block<T, VEC, TEAM, FAN>(a);
+        return;
+    }
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    VT* sm = reinterpret_cast<VT*>(smem_raw);   // [upc][TEAM] staged partials
+    VT* gbuf = sm + 256 + (threadIdx.x / 32) * (K3A_ROWS * 32);  // this warp's gather slots
+    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
+    const uint64_t u = (uint64_t)blockIdx.x * a.upc + tu;
+    const bool active = tu < a.upc && u < a.units;
+    uint64_t b = 0, e = 0;
+    uint32_t v = 0;
+    uint8_t f = 0;
+    if (active) {
+        b = __ldg(a.part_ptr + u);
+        e = __ldg(a.part_ptr + u + 1);
+        v = __ldg(a.part2node + u);
+        f = __ldg(a.uflags + u);
+    }
+    if (active && a.epi) {
+        if (a.epi & EPI_SCALE) prefetch_l1(a.scale + v);
+        if ((a.epi & EPI_SELF) && a.sw) prefetch_l1(a.sw + v);
+    }
+    if (a.pf && threadIdx.x < 32) {  // metadata look-ahead, as in K3
+        const uint64_t f0 = ((uint64_t)blockIdx.x + a.pf) * a.upc;
+        if (f0 < a.units) {
+            const uint32_t l = threadIdx.x;
+            const uint64_t cnt = a.units - f0 < (uint64_t)a.upc ? a.units - f0 : (uint64_t)a.upc;
+            if ((uint64_t)l * 16 <= cnt) prefetch_l2(a.part_ptr + f0 + (uint64_t)l * 16);
+            if ((uint64_t)l * 32 < cnt) prefetch_l2(a.part2node + f0 + (uint64_t)l * 32);
+            if ((uint64_t)l * 128 < cnt) prefetch_l2(a.uflags + f0 + (uint64_t)l * 128);
+        }
+    }
+    const bool direct = (f & (UF_LEADER | UF_RUN_END)) == (UF_LEADER | UF_RUN_END) && !(f & UF_SPLIT);
+    const bool staged = active && !direct;
+    const bool need_smem = __syncthreads_or(staged);
+    const uint32_t off = lane * VEC;
+    const bool ok = lane < a.nvec;
+    VT acc;
+    vzero(acc);
+    gather_async<T, VEC, TEAM, EW>(a, b, e, lane, off, ok, acc, gbuf);
+    if (active && direct && ok) store_final<T, VEC, FAN>(a, v, off, acc);
+    if (need_smem) {
+        if (staged) sm[tu * TEAM + lane] = acc;
+        __syncthreads();
+        if (staged && (f & UF_LEADER)) {
+            VT r;
+            vzero(r);
+            uint32_t t2 = tu;
+            uint8_t f2 = f;
+            for (;;) {
+                vadd(r, sm[t2 * TEAM + lane]);
+                if (f2 & UF_RUN_END) break;
+                ++t2;
+                f2 = __ldg(a.uflags + u + (t2 - tu));
+            }
+            if (f & UF_SPLIT) {
+                const uint32_t c = __ldg(a.cidx + u);
+                if (ok) stv<T, VEC>(static_cast<T*>(a.carry) + (size_t)c * a.dim + off, r);
+                carry_arrive<T, VEC, TEAM, FAN>(a, c, lane);
+            } else if (ok) {
+                store_final<T, VEC, FAN>(a, v, off, r);
+            }
+        }
     }
 }
 
@@ -516,47 +702,90 @@ Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const
     return s;
 }
 
+// K3A launch (cp.async row gather into shared memory): true when it ran.
+template <class T, int VEC, int TEAM, bool EW, bool FAN>
+void launch_k3a_v(gnna_ctx* ctx, AggArgs& a, uint64_t grid) {
+    auto kern = k3a_aggregate<T, VEC, TEAM, EW, FAN>;
+    const size_t smem = (256 + 8 * K3A_ROWS * 32) * sizeof(Vec<T, VEC>);
+    static bool attr = false;
+    if (!attr) {
+        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
+    gnna::launched(ctx, "k3a_aggregate");
+}
+
+// K3A is used for narrow fp64 rows (one 16-byte chunk per lane): there the
+// plain K3's register-held gather caps rows in flight (r02 A/B, C3 fp64:
+// 0.081 vs 0.109 ms); narrow fp32 rows measured even (0.0563 both) and the
+// weighted gather slower (0.094 vs 0.079), so fp32 keeps K3.  GNNA_K3A=0/2
+// forces K3 / K3A everywhere it applies (A/B).
+template <class T, int VEC, int TEAM>
+bool k3a_applies(const AggArgs& a, uint32_t kmax) {
+    if constexpr (TEAM >= 2 && TEAM <= 8 && sizeof(T) * VEC == 16) {
+        static const int mode = std::getenv("GNNA_K3A") ? std::atoi(std::getenv("GNNA_K3A")) : 1;
+        if (mode == 0 || kmax != 1 || a.kpl != 1 || a.upc * TEAM > 256) return false;
+        if (a.nw && (a.npeer || a.mc)) return false;
+        return mode == 2 || std::is_same<T, double>::value;
+    } else {
+        (void)a; (void)kmax;
+        return false;
+    }
+}
+
 template <class T, int VEC, int TEAM>
 void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, const gnna_plan* plan) {
+    const bool fan = a.npeer || a.mc;
+    constexpr bool kEW = std::is_same<T, float>::value;  // weighted gathers: fp32 path only
+    if (fan && a.nw) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_fanout: node weights are not supported");
+    // split-node carries are combined by their last writer, zero-degree rows by
+    // trailing blocks: one launch per aggregation
+    a.unit_blocks = grid;
+    a.nempty = plan->nempty;
+    a.empty_rows = plan->fix_nodes.get() + plan->nsplit;
+    a.carry_split = plan->carry_split.get();
+    a.split_cnt = plan->split_cnt.get();
+    a.split_node = plan->fix_nodes.get();
+    a.split_first = plan->fix_first.get();
+    a.split_count = plan->fix_count.get();
+    if (k3a_applies<T, VEC, TEAM>(a, kmax)) {
+        if constexpr (TEAM >= 2 && TEAM <= 8 && sizeof(T) * VEC == 16) {
+            const uint64_t total = grid + (a.nempty + 256 / TEAM - 1) / (256 / TEAM);
+            if (total > 0x7fffffffull) gnna::raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
+            if (fan) launch_k3a_v<T, VEC, TEAM, false, true>(ctx, a, total);
+            else if (a.nw && kEW) launch_k3a_v<T, VEC, TEAM, kEW, false>(ctx, a, total);
+            else launch_k3a_v<T, VEC, TEAM, false, false>(ctx, a, total);
+        }
+        return;
+    }
     const size_t smem = (size_t)a.upc * kmax * TEAM * sizeof(Vec<T, VEC>);
     const unsigned threads = (a.upc * TEAM + 31) / 32 * 32;  // whole warps (gather_team is warp-collective)
-    const bool fan = a.npeer || a.mc;
-    if (grid) {
-        constexpr bool kEW = std::is_same<T, float>::value;  // weighted gathers: fp32 path only
-        if (fan) {  // fused all-gather: fp32 and fp64, unweighted gathers
-            if (a.nw) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_fanout: node weights are not supported");
-            if (kmax == 1)
-                k3_aggregate<T, VEC, TEAM, 1, false, true><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-            else if (kmax == 2)
-                k3_aggregate<T, VEC, TEAM, 2, false, true><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-            else
-                k3_aggregate<T, VEC, TEAM, 4, false, true><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-        } else if (a.nw && kEW) {
-            if (kmax == 1)
-                k3_aggregate<T, VEC, TEAM, 1, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-            else if (kmax == 2)
-                k3_aggregate<T, VEC, TEAM, 2, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-            else
-                k3_aggregate<T, VEC, TEAM, 4, kEW><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-        } else if (kmax == 1)
-            k3_aggregate<T, VEC, TEAM, 1, false><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+    const uint64_t total = grid + (a.nempty + threads / TEAM - 1) / (threads / TEAM);
+    if (!total) return;
+    if (total > 0x7fffffffull) gnna::raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
+    const unsigned g = (unsigned)total;
+    if (fan) {  // fused all-gather: fp32 and fp64, unweighted gathers
+        if (kmax == 1)
+            k3_aggregate<T, VEC, TEAM, 1, false, true><<<g, threads, smem, ctx->stream>>>(a);
         else if (kmax == 2)
-            k3_aggregate<T, VEC, TEAM, 2, false><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
+            k3_aggregate<T, VEC, TEAM, 2, false, true><<<g, threads, smem, ctx->stream>>>(a);
         else
-            k3_aggregate<T, VEC, TEAM, 4, false><<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
-        gnna::launched(ctx, "k3_aggregate");
-    }
-    const uint64_t nfix = plan->nsplit + plan->nempty;
-    if (nfix) {
-        const unsigned fgrid = (unsigned)((nfix + 256 / TEAM - 1) / (256 / TEAM));
-        if (fan)
-            k3b_fixup<T, VEC, TEAM, true><<<fgrid, 256, 0, ctx->stream>>>(
-                a, plan->fix_nodes.get(), plan->fix_first.get(), plan->fix_count.get(), plan->nsplit, nfix);
+            k3_aggregate<T, VEC, TEAM, 4, false, true><<<g, threads, smem, ctx->stream>>>(a);
+    } else if (a.nw && kEW) {
+        if (kmax == 1)
+            k3_aggregate<T, VEC, TEAM, 1, kEW><<<g, threads, smem, ctx->stream>>>(a);
+        else if (kmax == 2)
+            k3_aggregate<T, VEC, TEAM, 2, kEW><<<g, threads, smem, ctx->stream>>>(a);
         else
-            k3b_fixup<T, VEC, TEAM><<<fgrid, 256, 0, ctx->stream>>>(a, plan->fix_nodes.get(), plan->fix_first.get(),
-                                                                   plan->fix_count.get(), plan->nsplit, nfix);
-        gnna::launched(ctx, "k3b_fixup");
-    }
+            k3_aggregate<T, VEC, TEAM, 4, kEW><<<g, threads, smem, ctx->stream>>>(a);
+    } else if (kmax == 1)
+        k3_aggregate<T, VEC, TEAM, 1, false><<<g, threads, smem, ctx->stream>>>(a);
+    else if (kmax == 2)
+        k3_aggregate<T, VEC, TEAM, 2, false><<<g, threads, smem, ctx->stream>>>(a);
+    else
+        k3_aggregate<T, VEC, TEAM, 4, false><<<g, threads, smem, ctx->stream>>>(a);
+    gnna::launched(ctx, "k3_aggregate");
 }
 
 template <class T, int VEC>
@@ -599,7 +828,7 @@ void launch_k4(gnna_ctx* ctx, AggArgs& a, const Shape& s) {
 
 namespace gnna {
 
-// Scheduled aggregation over a plan (K3 + K3b) with the optional epilogue
+// Scheduled aggregation over a plan (one K3 / K3A launch) with the optional epilogue
 // and per-edge weights of gnna_agg_opts (o may be null).
 void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
                         const gnna_agg_opts* o, void* const* peers, uint32_t npeer, void* mc) {
@@ -659,8 +888,7 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
         a.pf = pf_env >= 0 ? (uint32_t)pf_env : (uint32_t)(3 * ctx->num_sms);  // ~ the resident CTAs of one wave
     }
     if (plan->G == 0 && plan->nempty == 0) return;
-    const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;
-    if (grid > 0x7fffffffull) raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
+    const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;  // unit blocks
     if (dtype == GNNA_F32) {
         if (s.vec == 4) launch_k3<float, 4>(ctx, a, s, grid, plan);
         else launch_k3<float, 1>(ctx, a, s, grid, plan);

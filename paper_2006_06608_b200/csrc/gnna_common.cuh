@@ -186,12 +186,10 @@ struct gnna_plan {
     gnna::DevBuf<uint32_t> fix_first;  // nsplit: first carry index
     gnna::DevBuf<uint32_t> fix_count;  // nsplit: carries per split node
     mutable gnna::DevBuf<uint8_t> carry;  // ncarry * dim * 8 bytes (grown for wider dims)
-    gnna::DevBuf<uint32_t> tile_counter;  // K3P dynamic tile scheduler (reset per launch)
+    gnna::DevBuf<uint32_t> carry_split;   // ncarry: carry slot -> split-node index
+    gnna::DevBuf<uint32_t> split_cnt;     // nsplit: K3 arrival counters (zero between launches)
 };
 
-// part_ptr / part2node / uflags carry this many entries of slack past G, so
-// K3P's 16-byte bulk copies of a tile's metadata never leave the allocation.
-constexpr uint64_t kPlanPad = 32;
 
 // Unit flag bits (plan.cu builds them, aggregate.cu consumes them).
 enum : uint8_t {

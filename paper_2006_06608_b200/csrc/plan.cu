@@ -119,6 +119,14 @@ __global__ void k2_fix_lists(const uint64_t* __restrict__ ustart, uint32_t r0, u
     }
 }
 
+// carry slot -> split-node index (the last-writer combine in K3 looks up
+// its node's first slot and slot count through it).
+__global__ void k2_carry_split(const uint32_t* __restrict__ first, const uint32_t* __restrict__ count, uint64_t nsplit,
+                               uint32_t* __restrict__ carry_split) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nsplit; k += (uint64_t)gridDim.x * blockDim.x)
+        for (uint32_t j = 0; j < count[k]; ++j) carry_split[first[k] + j] = (uint32_t)k;
+}
+
 // Consecutive-run validation for arbitrary targets (memplan.cpp:15-29):
 // the first position whose target already had an earlier run.
 __global__ void k2_first_run(const uint32_t* __restrict__ t, uint64_t G, unsigned long long* __restrict__ first) {
@@ -276,16 +284,11 @@ gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
             const uint64_t G = unit_starts(ctx, d_row_ptr, row_begin, rows, p->ngs, us);
             if (G >= (1ull << 32)) gnna::raise(GNNA_ERR_DOMAIN, "plan: more than 2^32 workload units");
             plan->G = G;
-            plan->part_ptr = DevBuf<uint64_t>(G + 1 + kPlanPad, s);
-            plan->part2node = DevBuf<uint32_t>(G + kPlanPad, s);
+            plan->part_ptr = DevBuf<uint64_t>(G + 1, s);
+            plan->part2node = DevBuf<uint32_t>(G ? G : 1, s);
             plan->slot = DevBuf<uint8_t>(G ? G : 1, s);
             plan->leader = DevBuf<uint8_t>(G ? G : 1, s);
-            plan->uflags = DevBuf<uint8_t>(G + kPlanPad, s);
-            plan->tile_counter = DevBuf<uint32_t>(1, s);
-            // the slack is never read as data, but keep it defined (sanitizer initcheck)
-            GNNA_CUDA(cudaMemsetAsync(plan->part_ptr.get() + G + 1, 0, kPlanPad * 8, s));
-            GNNA_CUDA(cudaMemsetAsync(plan->part2node.get() + G, 0, kPlanPad * 4, s));
-            GNNA_CUDA(cudaMemsetAsync(plan->uflags.get() + G, 0, kPlanPad, s));
+            plan->uflags = DevBuf<uint8_t>(G ? G : 1, s);
             plan->cidx = DevBuf<uint32_t>(G ? G : 1, s);
             if (rows) {
                 k1_write<<<gnna::grid_for((uint64_t)rows * 32, 256), 256, 0, s>>>(
@@ -346,6 +349,14 @@ gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
                 }
             }
             if (plan->ncarry) plan->carry = DevBuf<uint8_t>(plan->ncarry * (uint64_t)p->dim * 8, s);
+            plan->carry_split = DevBuf<uint32_t>(plan->ncarry ? plan->ncarry : 1, s);
+            plan->split_cnt = DevBuf<uint32_t>(plan->nsplit ? plan->nsplit : 1, s);
+            GNNA_CUDA(cudaMemsetAsync(plan->split_cnt.get(), 0, (plan->nsplit ? plan->nsplit : 1) * 4, s));
+            if (plan->nsplit) {
+                k2_carry_split<<<gnna::grid_for(plan->nsplit, 256), 256, 0, s>>>(
+                    plan->fix_first.get(), plan->fix_count.get(), plan->nsplit, plan->carry_split.get());
+                gnna::launched(ctx, "k2_carry_split");
+            }
             GNNA_CUDA(cudaStreamSynchronize(s));
         } catch (...) {
             delete plan;
