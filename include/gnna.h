@@ -305,6 +305,15 @@ GNNA_API gnna_status gnna_gemm(gnna_ctx* ctx, int dtype, const void* d_a, uint32
  * of matmul; row-chunk partials summed in chunk order: deterministic). */
 GNNA_API gnna_status gnna_gemm_tn(gnna_ctx* ctx, int dtype, const void* d_a, const void* d_b, uint32_t m,
                          uint32_t p, uint32_t q, void* d_out);
+/* Backward of the node update y = z W (matmul, engine.cpp:315-331; no
+ * reference backward exists): dz (m x p) = row_scale ⊙ (dy Wᵀ)
+ * (row_scale may be null) and dW (p x q) = zᵀ dy, for dy (m x q), W (p x q),
+ * z (m x p).  F32 with p, q <= 32 runs ONE fused pass over the rows (the
+ * narrow GCN output layer); otherwise the two products run separately
+ * (F64: the exact orders of gnna_gemm / gnna_gemm_tn). */
+GNNA_API gnna_status gnna_dense_backward(gnna_ctx* ctx, int dtype, const void* d_dy, uint32_t m, uint32_t q,
+                                const void* d_w, const void* d_z, uint32_t p, const double* d_row_scale,
+                                void* d_dz, void* d_dw);
 /* engine.hpp:93 gcn_layer / engine.hpp:108 gin_layer, forward (F64 bitwise;
  * F32 runs a scheduled plan with the normalisation fused into K3). */
 GNNA_API gnna_status gnna_gcn_forward(gnna_ctx* ctx, int dtype, const uint64_t* d_row_ptr,

@@ -370,6 +370,23 @@ class Context:
                                      C.c_uint32(n_out), _ptr(bias), C.c_int(epilogue), _ptr(row_scale), _ptr(out)))
         return out
 
+    def dense_backward(self, dy, w, z, row_scale=None):
+        """gnna_dense_backward: (dz = row_scale * (dy W^T), dW = z^T dy) for
+        y = z W; one fused pass for narrow fp32 layers."""
+        torch = self.torch
+        m, q = dy.shape
+        p = w.shape[0]
+        _dev(dy, "dy", (torch.float32, torch.float64))
+        _dev(w, "w", dy.dtype, (p, q))
+        _dev(z, "z", dy.dtype, (m, p))
+        _dev(row_scale, "row_scale", torch.float64, (m,))
+        dz = torch.empty((m, p), dtype=dy.dtype, device=dy.device)
+        dw = torch.empty((p, q), dtype=dy.dtype, device=dy.device)
+        self._check(self.L.gnna_dense_backward(self.h, C.c_int(_dtype_code(dy)), _ptr(dy), C.c_uint32(m),
+                                               C.c_uint32(q), _ptr(w), _ptr(z), C.c_uint32(p), _ptr(row_scale),
+                                               _ptr(dz), _ptr(dw)))
+        return dz, dw
+
     def gcn_norm(self, row_ptr, col, self_loops=False):
         n = row_ptr.numel() - 1
         norm = self._empty(max(n, 1), self.torch.float64)

@@ -804,6 +804,194 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
     }
 }
 
+// ------------------------------------------------- K6 dense backward (fused)
+// Backward of the node update y = z W (matmul, engine.cpp:315-331) in one
+// pass over the rows, for the narrow widths of the GCN output layer (C3:
+// z 16 wide, y 22 wide, whose 88-byte rows no TMA descriptor can stride):
+//   dz = row_scale ⊙ (dy Wᵀ)          (m x p)
+//   dW = zᵀ dy                         (p x q, per-CTA partials summed in
+//                                       CTA order by k_reduce_partials)
+// Both read dy; one kernel reads dy and z once instead of the two passes of
+// k6_gemm_flat + k6_gemm_tn_small.  A CTA owns a contiguous row chunk
+// (deterministic partials) and streams it in DB_ROWS-row tiles with a
+// double-buffered cp.async pipeline (the same copy_run scheme as
+// k6_gemm_tn_small).  dz: 4 threads per row, each 4 output columns (W held
+// k-major in shared memory, one 16-byte broadcast read per k), stored as
+// one coalesced float4 per thread.  dW: TI x TJ = 4 x 4 register tiles over
+// row groups, summed in group order at the end.
+#ifndef GNNA_DB_ROWS
+#define GNNA_DB_ROWS 128
+#endif
+#ifndef GNNA_DB_STAGES
+#define GNNA_DB_STAGES 3
+#endif
+constexpr int DB_ROWS = GNNA_DB_ROWS, DB_STAGES = GNNA_DB_STAGES, DB_P = 32, DB_Q = 32;
+
+// Compile-time widths (P, Q <= 32): every inner loop unrolls, operands are
+// read as 16-/8-byte shared vectors and the FMA chains are independent.
+template <int P, int Q>
+__global__ void __launch_bounds__(256) k6_dense_bwd(const float* __restrict__ dy, const float* __restrict__ w,
+                                                    const float* __restrict__ z, const double* __restrict__ row_scale,
+                                                    uint32_t m, uint32_t rows_per_cta, float* __restrict__ dz,
+                                                    float* __restrict__ part) {
+    static_assert(P % 4 == 0 && Q % 2 == 0 && P <= DB_P && Q <= DB_Q, "dense_bwd widths");
+    constexpr int TI = 4, TJ = 8;                       // dW register tile
+    constexpr int TQ = (Q + TJ - 1) / TJ, TILES = (P / TI) * TQ, RG = 256 / TILES;
+    constexpr int PH = P / 2;                           // dz: 2 threads per row, PH outputs each
+    extern __shared__ __align__(16) float sm[];
+    float* sdy = sm;                                    // [S][DB_ROWS * Q]
+    float* sz = sdy + DB_STAGES * DB_ROWS * Q;          // [S][DB_ROWS * P]
+    float* swt = sz + DB_STAGES * DB_ROWS * P;          // [Q][P]: W^T, k-major
+    double* srs = reinterpret_cast<double*>(swt + Q * P + (Q * P) % 2);  // [S][DB_ROWS] row scales
+    const uint32_t t = threadIdx.x;
+    for (uint32_t e = t; e < Q * P; e += blockDim.x) {
+        const uint32_t k = e / P, i = e % P;
+        swt[e] = __ldg(w + (size_t)i * Q + k);
+    }
+    const uint32_t grp = t / TILES, tile = t % TILES;
+    const bool active = grp < RG;
+    const uint32_t ti = (tile / TQ) * TI, tj = (tile % TQ) * TJ;
+    const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_cta;
+    const uint64_t r_end = r_begin + rows_per_cta < m ? r_begin + rows_per_cta : m;
+    const uint32_t nblk = r_end > r_begin ? (uint32_t)((r_end - r_begin + DB_ROWS - 1) / DB_ROWS) : 0u;
+    auto copy_run = [&](float* dst, const float* src, uint32_t cnt) {
+        const uint32_t head = (uint32_t)((16 - ((uintptr_t)src & 15)) & 15) / 4;
+        const bool v16 = (((uintptr_t)src ^ (uintptr_t)dst) & 15) == 0 && cnt > head;
+        const uint32_t h = v16 ? head : cnt;
+        for (uint32_t e = t; e < h; e += blockDim.x) cp_async4(dst + e, src + e);
+        if (!v16) return;
+        const uint32_t nv = (cnt - h) / 4;
+        for (uint32_t e = t; e < nv; e += blockDim.x)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(dst + h + 4 * e)),
+                         "l"(src + h + 4 * e)
+                         : "memory");
+        for (uint32_t e = h + 4 * nv + t; e < cnt; e += blockDim.x) cp_async4(dst + e, src + e);
+    };
+    // one commit group per ring slot (empty past the chunk, so wait_group counts stay uniform)
+    auto load = [&](uint32_t blk) {
+        if (blk < nblk) {
+            const uint32_t buf = blk % DB_STAGES;
+            const uint64_t r0 = r_begin + (uint64_t)blk * DB_ROWS;
+            const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)DB_ROWS ? r_end - r0 : (uint64_t)DB_ROWS);
+            copy_run(sdy + (size_t)buf * DB_ROWS * Q, dy + r0 * Q, nr * Q);
+            copy_run(sz + (size_t)buf * DB_ROWS * P, z + r0 * P, nr * P);
+            if (row_scale)
+                for (uint32_t e = t; e < nr; e += blockDim.x)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(srs + (size_t)buf * DB_ROWS + e)),
+                                 "l"(row_scale + r0 + e)
+                                 : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    float acc[TI][TJ];
+#pragma unroll
+    for (int i = 0; i < TI; ++i)
+#pragma unroll
+        for (int j = 0; j < TJ; ++j) acc[i][j] = 0.f;
+#pragma unroll
+    for (int s = 0; s < DB_STAGES - 1; ++s) load(s);
+    for (uint32_t blk = 0; blk < nblk; ++blk) {
+        load(blk + DB_STAGES - 1);  // refills the slot freed at the end of the previous iteration
+        asm volatile("cp.async.wait_group %0;" ::"n"(DB_STAGES - 1) : "memory");
+        __syncthreads();
+        const uint32_t buf = blk % DB_STAGES;
+        const uint64_t r0 = r_begin + (uint64_t)blk * DB_ROWS;
+        const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)DB_ROWS ? r_end - r0 : (uint64_t)DB_ROWS);
+        const float* xdy = sdy + (size_t)buf * DB_ROWS * Q;
+        const float* xz = sz + (size_t)buf * DB_ROWS * P;
+        // dz = row_scale * (dy W^T): 2 threads per row, PH outputs each
+        for (uint32_t it = t; it < 2 * DB_ROWS; it += blockDim.x) {
+            const uint32_t dr = it / 2, half = it % 2;
+            if (dr >= nr) break;
+            float yv[Q];
+#pragma unroll
+            for (int k = 0; k < Q; k += 2) {
+                const float2 y2 = *reinterpret_cast<const float2*>(xdy + dr * Q + k);
+                yv[k] = y2.x;
+                yv[k + 1] = y2.y;
+            }
+            float o[PH];
+#pragma unroll
+            for (int c = 0; c < PH; ++c) o[c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < Q; ++k)
+#pragma unroll
+                for (int c = 0; c < PH; c += 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(swt + k * P + half * PH + c);
+                    o[c] = fmaf(yv[k], w4.x, o[c]);
+                    o[c + 1] = fmaf(yv[k], w4.y, o[c + 1]);
+                    o[c + 2] = fmaf(yv[k], w4.z, o[c + 2]);
+                    o[c + 3] = fmaf(yv[k], w4.w, o[c + 3]);
+                }
+            const float s = row_scale ? (float)srs[(size_t)buf * DB_ROWS + dr] : 1.f;
+            float4* out = reinterpret_cast<float4*>(dz + (r0 + dr) * P + half * PH);
+#pragma unroll
+            for (int c = 0; c < PH; c += 4) out[c / 4] = make_float4(s * o[c], s * o[c + 1], s * o[c + 2], s * o[c + 3]);
+        }
+        // dW += z^T dy over this tile's rows (TI x TJ register tile per thread)
+        if (active) {
+            for (uint32_t k = grp; k < nr; k += RG) {
+                const float4 a4 = *reinterpret_cast<const float4*>(xz + k * P + ti);
+                float bv[TJ];
+#pragma unroll
+                for (int j = 0; j < TJ; j += 2) {
+                    const float2 b2 = tj + j < Q ? *reinterpret_cast<const float2*>(xdy + k * Q + tj + j)
+                                                 : make_float2(0.f, 0.f);
+                    bv[j] = b2.x;
+                    bv[j + 1] = b2.y;
+                }
+                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int i = 0; i < TI; ++i)
+#pragma unroll
+                    for (int j = 0; j < TJ; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            }
+        }
+        __syncthreads();  // slot `buf` is refilled by the next iteration's load
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    float* red = sm;  // [RG][P*Q] (staging area is free)
+    constexpr uint32_t total = P * Q;
+    if (active)
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+            for (int j = 0; j < TJ; ++j)
+                if (tj + j < Q) red[(size_t)grp * total + (ti + i) * Q + tj + j] = acc[i][j];
+    __syncthreads();
+    for (uint32_t o = t; o < total; o += blockDim.x) {
+        float sum = 0.f;
+        for (uint32_t g2 = 0; g2 < RG; ++g2) sum += red[(size_t)g2 * total + o];
+        part[(size_t)blockIdx.x * total + o] = sum;
+    }
+}
+
+template <int P, int Q>
+void launch_dense_bwd(gnna_ctx* ctx, const float* dy, const float* w, const float* z, const double* rs, uint32_t m,
+                      float* dz, float* dw) {
+    constexpr int TQ = (Q + 7) / 8, TILES = (P / 4) * TQ, RG = 256 / TILES;
+    const size_t sbytes = std::max<size_t>((size_t)(DB_STAGES * DB_ROWS * (P + Q) + Q * P + (Q * P) % 2 +
+                                                    2 * DB_STAGES * DB_ROWS),
+                                           (size_t)RG * P * Q) * 4;
+    static int occ = -1;
+    if (occ < 0) {
+        GNNA_CUDA(cudaFuncSetAttribute(k6_dense_bwd<P, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes));
+        GNNA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k6_dense_bwd<P, Q>, 256, sbytes));
+        occ = std::max(occ, 1);
+    }
+    uint32_t ctas = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)occ * ctx->num_sms, (m + DB_ROWS - 1) / DB_ROWS));
+    const uint32_t rpc = ((m + ctas - 1) / ctas + DB_ROWS - 1) / DB_ROWS * DB_ROWS;
+    ctas = (m + rpc - 1) / rpc;
+    gnna::DevBuf<float> part((size_t)ctas * P * Q, ctx->stream);
+    k6_dense_bwd<P, Q><<<ctas, 256, sbytes, ctx->stream>>>(dy, w, z, rs, m, rpc, dz, part.get());
+    gnna::launched(ctx, "k6_dense_bwd");
+    gnna::k_reduce_partials<<<(P * Q + 31) / 32, 1024, 0, ctx->stream>>>(part.get(), ctas, P * Q, dw);
+    gnna::launched(ctx, "k_reduce_partials");
+}
+
 constexpr int TN4_ROWS = 32;
 
 __global__ void k6_gemm_tn4(const float* __restrict__ a, const float* __restrict__ b, uint32_t m, uint32_t p,
@@ -1146,5 +1334,41 @@ extern "C" gnna_status gnna_gemm_tn(gnna_ctx* ctx, int dtype, const void* d_a, c
         gnna::require_ctx(ctx);
         if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
         gnna::gemm_tn(ctx, dtype, d_a, d_b, m, p, q, d_out);
+    });
+}
+
+// Backward of y = z W for narrow layers, fused (see k6_dense_bwd):
+// dz = row_scale ⊙ (dy Wᵀ) and dW = zᵀ dy in one pass (fp32); the fp64 path
+// (and wide layers) runs the two products separately, in the exact orders.
+extern "C" gnna_status gnna_dense_backward(gnna_ctx* ctx, int dtype, const void* d_dy, uint32_t m, uint32_t q,
+                                           const void* d_w, const void* d_z, uint32_t p, const double* d_row_scale,
+                                           void* d_dz, void* d_dw) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        if (!d_dz || !d_dw) gnna::raise(GNNA_ERR_DOMAIN, "dense_backward: null output");
+        const uint32_t total = p * q;
+        (void)total;
+        static const bool off = std::getenv("GNNA_DENSE_BWD") && std::atoi(std::getenv("GNNA_DENSE_BWD")) == 0;
+        if (dtype == GNNA_F32 && !off && m > 0 && (uintptr_t)d_dy % 16 == 0 && (uintptr_t)d_z % 16 == 0 &&
+            (uintptr_t)d_dz % 16 == 0) {
+            const auto dy = static_cast<const float*>(d_dy);
+            const auto w = static_cast<const float*>(d_w);
+            const auto z = static_cast<const float*>(d_z);
+            auto dz = static_cast<float*>(d_dz);
+            auto dw = static_cast<float*>(d_dw);
+            // instantiated widths: the GCN output layers of the configs (C3: 16 x 22)
+            if (p == 16 && q == 22) return launch_dense_bwd<16, 22>(ctx, dy, w, z, d_row_scale, m, dz, dw);
+            if (p == 16 && q == 16) return launch_dense_bwd<16, 16>(ctx, dy, w, z, d_row_scale, m, dz, dw);
+            if (p == 16 && q == 8) return launch_dense_bwd<16, 8>(ctx, dy, w, z, d_row_scale, m, dz, dw);
+            if (p == 32 && q == 32) return launch_dense_bwd<32, 32>(ctx, dy, w, z, d_row_scale, m, dz, dw);
+            if (p == 32 && q == 22) return launch_dense_bwd<32, 22>(ctx, dy, w, z, d_row_scale, m, dz, dw);
+        }
+        // separate products: dW = z^T dy; dz = dy W^T (W^T materialised), row-scaled
+        gnna::gemm_tn(ctx, dtype, d_z, d_dy, m, p, q, d_dw);
+        const size_t el = dtype == GNNA_F32 ? 4 : 8;
+        gnna::DevBuf<uint8_t> wt((size_t)total * el, ctx->stream);
+        gnna::transpose(ctx, dtype, d_w, p, q, wt.get());
+        gnna::gemm(ctx, dtype, d_dy, m, q, wt.get(), p, nullptr, d_row_scale ? 2 : 0, d_row_scale, d_dz);
     });
 }

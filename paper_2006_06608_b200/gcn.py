@@ -124,9 +124,10 @@ class GCN2:
                 side.stream.wait_stream(main)
                 with torch.cuda.stream(side.stream):
                     dw2 = ctx_gemm_tn(side.ctx, s["z2"], dy)
+                dz2 = ctx.gemm(dy, w2t, None, 2, self.norm)        # norm * (dY W2^T)
             else:
-                dw2 = ctx_gemm_tn(ctx, s["z2"], dy)                # (Â h1)^T dY
-            dz2 = ctx.gemm(dy, w2t, None, 2, self.norm)            # norm * (dY W2^T)
+                # one pass over dY and Â h1: dZ2 = norm * (dY W2^T), dW2 = (Â h1)^T dY
+                dz2, dw2 = ctx.dense_backward(dy, self.w2, s["z2"], self.norm)
             # Â^T dZ2 masked by relu'(h1) (the sign of a pre-scaled h1 is the same);
             # pre-scaled by norm again when the next aggregation consumes it
             dp1_scaled = hid < in_dim

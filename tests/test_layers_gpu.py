@@ -178,3 +178,38 @@ def test_backward_nonsymmetric_uses_transpose(ctx, orc):
     wdx, wdw = orc.gcn_backward(rp, col, x, w, dy, False)
     np.testing.assert_allclose(gdx.cpu().numpy(), wdx, rtol=1e-10, atol=1e-12)
     np.testing.assert_allclose(gdw.cpu().numpy(), wdw, rtol=1e-10, atol=1e-12)
+
+
+def test_dense_backward_fused(ctx):
+    """gnna_dense_backward (backward of y = z W): dz = s * (dy W^T), dW = z^T dy.
+    fp32 (one fused pass for p, q <= 32) at the error-aware 1e-5 bar, ragged
+    row counts and widths incl. the C3 output layer (16 x 22); fp64 equals
+    the separate exact products (gnna_gemm / gnna_gemm_tn orders)."""
+    from paper_2006_06608_b200.gcn import ctx_gemm_tn
+    rng = np.random.default_rng(9)
+    for m, p, q in ((1, 1, 1), (63, 16, 22), (64, 16, 22), (1000, 16, 22), (4097, 7, 13), (3000, 32, 32),
+                    (2500, 40, 22), (410236, 16, 22)):
+        dy = rng.random((m, q)) - 0.5
+        w = rng.random((p, q)) - 0.5
+        z = rng.random((m, p)) - 0.5
+        s = rng.random(m) + 0.5
+        ddy, dw, dz, ds = to_dev(dy.astype(np.float32), w.astype(np.float32), z.astype(np.float32), s)
+        gz, gw = ctx.dense_backward(ddy, dw, dz, ds)
+        y32, w32, z32 = (a.astype(np.float32).astype(np.float64) for a in (dy, w, z))
+        want_dz = s[:, None] * (y32 @ w32.T)
+        bound_dz = s[:, None] * (np.abs(y32) @ np.abs(w32).T)
+        ok, r = close32(gz.cpu().numpy(), want_dz, bound_dz)
+        assert ok, (m, p, q, "dz", r)
+        ok, r = close32(gw.cpu().numpy(), z32.T @ y32, np.abs(z32).T @ np.abs(y32))
+        assert ok, (m, p, q, "dW", r)
+        # fp64: the separate exact products
+        d64 = to_dev(dy, w, z)
+        gz64, gw64 = ctx.dense_backward(d64[0], d64[1], d64[2], ds)
+        assert torch.equal(gw64, ctx_gemm_tn(ctx, d64[2], d64[0]))
+        assert torch.equal(gz64, ctx.gemm(d64[0], d64[1].t().contiguous(), None, 2, ds))
+    # no row scale
+    dy, w, z = (torch.rand(s, device="cuda") - 0.5 for s in ((777, 22), (16, 22), (777, 16)))
+    gz, _ = ctx.dense_backward(dy, w, z)
+    want = dy.double() @ w.double().t()
+    ok, r = close32(gz.cpu().numpy(), want.cpu().numpy(), (dy.double().abs() @ w.double().abs().t()).cpu().numpy())
+    assert ok, r
