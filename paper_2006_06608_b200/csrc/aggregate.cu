@@ -379,6 +379,23 @@ __device__ __forceinline__ void empty_rows_block(const AggArgs& a) {
     for (uint32_t ch = lane; ch < a.nvec; ch += TEAM) store_final<T, VEC, FAN>(a, v, ch * VEC, z);
 }
 
+// Wide-row plans (TEAM > 8 or KMAX > 1): split nodes add their carries in
+// block order in a second launch (one team per node).
+template <class T, int VEC, int TEAM, bool FAN>
+__global__ void __launch_bounds__(256) k3b_split(AggArgs a, uint64_t nsplit) {
+    const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
+    const uint64_t k = (uint64_t)blockIdx.x * (256 / TEAM) + tu;
+    if (k >= nsplit) return;
+    const uint32_t v = a.split_node[k], first = a.split_first[k], cnt = a.split_count[k];
+    const T* cy = static_cast<const T*>(a.carry) + (size_t)first * a.dim;
+    for (uint32_t ch = lane; ch < a.nvec; ch += TEAM) {
+        Vec<T, VEC> acc;
+        vzero(acc);
+        for (uint32_t j = 0; j < cnt; ++j) vadd(acc, ldv<T, VEC>(cy + (size_t)j * a.dim + ch * VEC));
+        store_final<T, VEC, FAN>(a, v, ch * VEC, acc);
+    }
+}
+
 // ----------------------------------------------------------------- K3 ---
 template <class T, int VEC, int TEAM, int KMAX, bool EW, bool FAN = false>
 __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX, EW>::minb) k3_aggregate(AggArgs a) {
@@ -454,7 +471,11 @@ __global__ void __launch_bounds__(256, K3Tune<TEAM, KMAX, EW>::minb) k3_aggregat
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k)
                         if (L.ok[k]) stv<T, VEC>(cy + L.off[k], r[k]);
-                    if (k0 + KMAX >= a.kpl) carry_arrive<T, VEC, TEAM, FAN>(a, __ldg(a.cidx + u), lane);
+                    // rows of 16+ vectors leave the combine to k3b_split: inlining it
+                    // there costs the gather loop registers (same-box A/B, C4: fp32
+                    // 0.0513 -> 0.0533 ms, fp64 0.084 -> 0.094 ms), while for narrow
+                    // rows the saved launch wins (C3 0.0563 -> 0.0521 ms)
+                    if constexpr (KMAX == 1 && TEAM <= 8) carry_arrive<T, VEC, TEAM, FAN>(a, __ldg(a.cidx + u), lane);
                 } else {
 #pragma unroll
                     for (int k = 0; k < KMAX; ++k)
@@ -786,6 +807,14 @@ void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, con
     else
         k3_aggregate<T, VEC, TEAM, 4, false><<<g, threads, smem, ctx->stream>>>(a);
     gnna::launched(ctx, "k3_aggregate");
+    if ((kmax > 1 || TEAM > 8) && plan->nsplit) {
+        const unsigned sg = (unsigned)((plan->nsplit + 256 / TEAM - 1) / (256 / TEAM));
+        if (fan)
+            k3b_split<T, VEC, TEAM, true><<<sg, 256, 0, ctx->stream>>>(a, plan->nsplit);
+        else
+            k3b_split<T, VEC, TEAM, false><<<sg, 256, 0, ctx->stream>>>(a, plan->nsplit);
+        gnna::launched(ctx, "k3b_split");
+    }
 }
 
 template <class T, int VEC>
