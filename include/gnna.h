@@ -376,6 +376,22 @@ GNNA_API gnna_status gnna_build_mapping(gnna_ctx* ctx, const uint32_t* d_com, ui
 GNNA_API gnna_status gnna_degree_order(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
                                        uint32_t* d_old_to_new, uint32_t* d_new_to_old);
 /* renumber.cpp:148 mapping_from_vector (DOMAIN if not a permutation). */
+/* Hub rows kept in L2 WITHOUT renumbering (drop-in path: the caller's node
+ * order, and so the reference's summation tree, stay as they are).  Picks
+ * the k highest-degree nodes (ties by id: the gnna_degree_order keys) into
+ * d_hubs[k] and writes d_col_out = d_col with every entry that names a hub
+ * replaced by n + its hub slot; *hub_edges = entries replaced (the hubs'
+ * gather share).  A plan built over d_col_out reads a hub's row from rows
+ * [n, n + k) of an extended feature buffer whose tail holds copies of the
+ * hub rows (gnna_gather_rows): the same values in the same order, so the
+ * result is bit-identical, while the hot rows are one contiguous block that
+ * gnna_set_l2_window can pin (the reference renumbers for locality,
+ * renumber.cpp; this keeps its order and gets B200's L2). */
+GNNA_API gnna_status gnna_hub_remap(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n,
+                           uint32_t k, uint32_t* d_hubs, uint32_t* d_col_out, uint64_t* hub_edges);
+/* d_out[i][:] = d_x[d_rows[i]][:] for i < count. */
+GNNA_API gnna_status gnna_gather_rows(gnna_ctx* ctx, int dtype, const void* d_x, uint32_t dim,
+                             const uint32_t* d_rows, uint64_t count, void* d_out);
 GNNA_API gnna_status gnna_mapping_from_vector(gnna_ctx* ctx, const uint32_t* d_vec, uint32_t n,
                                      uint32_t* d_old_to_new, uint32_t* d_new_to_old);
 /* renumber.cpp:162 apply_mapping (CSR), output canonical (rows sorted). */

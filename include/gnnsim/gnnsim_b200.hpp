@@ -362,4 +362,18 @@ RunResult run_pipeline(const EdgeList& el, const RunConfig& config);
 // the GNNSIM_DEVICE environment variable).
 void set_device(int device);
 
+// ====================================================== B200 additions
+// Not in the reference API: introspection of the drop-in's device cache and
+// hub layout (see gnnsim_dropin.cpp).  GNNSIM_CACHE=0 / GNNSIM_HUB=0 turn
+// them off.
+namespace b200 {
+struct CallStats {
+    bool cache_hit = false;        // the graph's device CSR and plans were reused
+    std::uint32_t hub_rows = 0;    // rows served from the L2-pinned hub block (0: layout off)
+    std::uint64_t hub_edges = 0;   // CSR entries that gather a hub row
+};
+CallStats last_call_stats();       // of the calling thread's last aggregate_scheduled
+void clear_cache();                // drops the calling thread's cached graphs
+}  // namespace b200
+
 }  // namespace gnnsim

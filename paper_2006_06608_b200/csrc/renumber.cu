@@ -160,6 +160,38 @@ unsigned read_flag(gnna_ctx* ctx, const DevBuf<unsigned>& f) {
     return h;
 }
 
+// Hub rows in L2 without renumbering (gnna_hub_remap / gnna_gather_rows).
+__global__ void k7_hub_slots(const uint64_t* __restrict__ sorted_keys, uint32_t k, uint32_t* __restrict__ hubs,
+                             uint32_t* __restrict__ slot) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)(sorted_keys[i] & 0xffffffffu);
+        hubs[i] = v;
+        slot[v] = (uint32_t)i;
+    }
+}
+
+__global__ void k7_hub_remap(const uint32_t* __restrict__ col, uint64_t nnz, const uint32_t* __restrict__ slot,
+                             uint32_t n, uint32_t* __restrict__ out, unsigned long long* __restrict__ hits) {
+    unsigned long long c = 0;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < nnz; e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = col[e], s = slot[u];
+        out[e] = s == 0xffffffffu ? u : n + s;
+        c += s != 0xffffffffu;
+    }
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(hits, c);
+}
+
+template <class T>
+__global__ void k7_gather_rows(const T* __restrict__ x, uint32_t dim, const uint32_t* __restrict__ rows, uint64_t count,
+                               T* __restrict__ out) {
+    const uint64_t total = count * dim;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = i / dim, c = i - r * dim;
+        out[i] = x[(uint64_t)rows[r] * dim + c];
+    }
+}
+
 }  // namespace
 
 namespace gnna {
@@ -312,6 +344,54 @@ gnna_status gnna_apply_mapping_edges(gnna_ctx* ctx, const uint32_t* d_edges, uin
         k7_relabel_edges<<<gnna::grid_for(e, 256), 256, 0, s>>>(d_edges, e, n, d_old_to_new, d_out_edges, bad.get());
         gnna::launched(ctx, "k7_relabel_edges");
         if (read_flag(ctx, bad)) gnna::raise(GNNA_ERR_DOMAIN, "apply_mapping: edge endpoint out of range");
+    });
+}
+
+gnna_status gnna_hub_remap(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uint32_t* d_col, uint32_t n, uint32_t k,
+                           uint32_t* d_hubs, uint32_t* d_col_out, uint64_t* hub_edges) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (k > n) gnna::raise(GNNA_ERR_DOMAIN, "hub_remap: more hubs than nodes");
+        if ((uint64_t)n + k > 0xffffffffull) gnna::raise(GNNA_ERR_DOMAIN, "hub_remap: n + k must fit in 32 bits");
+        cudaStream_t s = ctx->stream;
+        uint64_t nnz = 0;
+        if (n) gnna::to_host(ctx, &nnz, d_row_ptr + n, 1);
+        DevBuf<uint32_t> slot(n ? n : 1, s);
+        DevBuf<unsigned long long> hits(1, s);
+        GNNA_CUDA(cudaMemsetAsync(slot.get(), 0xff, (size_t)(n ? n : 1) * 4, s));
+        GNNA_CUDA(cudaMemsetAsync(hits.get(), 0, 8, s));
+        if (k) {  // the k highest-degree nodes, ties by id (the gnna_degree_order keys)
+            DevBuf<uint64_t> keys(n, s);
+            k7_degree_keys<<<gnna::grid_for(n, 256), 256, 0, s>>>(d_row_ptr, n, keys.get());
+            gnna::launched(ctx, "k7_degree_keys");
+            gnna::sort_keys_u64(ctx, keys.get(), n, 64);
+            k7_hub_slots<<<gnna::grid_for(k, 256), 256, 0, s>>>(keys.get(), k, d_hubs, slot.get());
+            gnna::launched(ctx, "k7_hub_slots");
+        }
+        if (nnz) {
+            k7_hub_remap<<<gnna::grid_for(nnz, 256), 256, 0, s>>>(d_col, nnz, slot.get(), n, d_col_out, hits.get());
+            gnna::launched(ctx, "k7_hub_remap");
+        }
+        unsigned long long h = 0;
+        gnna::to_host(ctx, &h, hits.get(), 1);
+        if (hub_edges) *hub_edges = h;
+    });
+}
+
+gnna_status gnna_gather_rows(gnna_ctx* ctx, int dtype, const void* d_x, uint32_t dim, const uint32_t* d_rows,
+                             uint64_t count, void* d_out) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        const uint64_t total = count * dim;
+        if (!total) return;
+        if (dtype == GNNA_F32)
+            k7_gather_rows<float><<<gnna::grid_for(total, 256), 256, 0, ctx->stream>>>(
+                static_cast<const float*>(d_x), dim, d_rows, count, static_cast<float*>(d_out));
+        else
+            k7_gather_rows<double><<<gnna::grid_for(total, 256), 256, 0, ctx->stream>>>(
+                static_cast<const double*>(d_x), dim, d_rows, count, static_cast<double*>(d_out));
+        gnna::launched(ctx, "k7_gather_rows");
     });
 }
 

@@ -54,3 +54,15 @@ def test_reference_unit_suite_on_b200(suite):
     r = subprocess.run([_bin("unit_b200"), f"--test-suite={suite}"], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert re.search(r"\| 0 failed \|", r.stdout)
+
+
+@pytest.mark.gpu
+def test_dropin_cache_and_hub_layout():
+    """tests/cpp/dropin_check.cpp: a C++ caller of gnnsim::aggregate_scheduled
+    (fp64, host buffers).  The device-graph cache is hit on a repeated call
+    and missed after an in-place edit; the hub layout (hub rows copied into an
+    L2-pinned tail, no renumbering) engages on a 300k-node power-law graph
+    and its outputs and CostReports are bit-identical to the plain path for
+    all three strategies; features_close(., aggregate_oracle, 1e-12) holds."""
+    r = subprocess.run([_bin("dropin_check"), "check"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "dropin_check ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
