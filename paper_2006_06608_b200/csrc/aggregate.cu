@@ -720,6 +720,11 @@ Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const
     s.team = std::min<uint32_t>(t, 32);
     s.kpl = (nvec + s.team - 1) / s.team;
     s.kmax = s.kpl <= 1 ? 1 : (s.kpl <= 2 ? 2 : 4);
+    // fp64 rows of 4+ chunks per lane: two passes of KMAX 2 instead of one of
+    // KMAX 4, whose 8 double2 accumulators + row vectors spill at the 64-register
+    // cap (GNNA_K3_F64_KMAX4=1 restores one pass for A/B)
+    static const bool f64_k4 = std::getenv("GNNA_K3_F64_KMAX4") != nullptr;
+    if (elem == 8 && s.kmax == 4 && !f64_k4) s.kmax = 2;
     return s;
 }
 

@@ -73,8 +73,9 @@ static bool same(const CostReport& a, const CostReport& b) {
     } while (0)
 
 static int check() {
-    // x = 300k x 64 doubles (154 MB > L2): the hub layout engages on a power-law graph
-    CsrGraph g = to_csr(power_law(300000, 3000000, 11, true), true);
+    // x = 1M x 64 doubles (512 MB > L2): the 98k hub rows of the 48 MB window
+    // draw several times their uniform share of the gathers
+    CsrGraph g = to_csr(power_law(1000000, 5000000, 11, true), true);
     const FeatureMatrix x = random_features(g.num_nodes, 64, 12);
     KernelParams p;
     p.ngs = 64;

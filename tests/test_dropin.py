@@ -61,7 +61,7 @@ def test_dropin_cache_and_hub_layout():
     """tests/cpp/dropin_check.cpp: a C++ caller of gnnsim::aggregate_scheduled
     (fp64, host buffers).  The device-graph cache is hit on a repeated call
     and missed after an in-place edit; the hub layout (hub rows copied into an
-    L2-pinned tail, no renumbering) engages on a 300k-node power-law graph
+    L2-pinned tail, no renumbering) engages on a 1M-node power-law graph
     and its outputs and CostReports are bit-identical to the plain path for
     all three strategies; features_close(., aggregate_oracle, 1e-12) holds."""
     r = subprocess.run([_bin("dropin_check"), "check"], capture_output=True, text=True, timeout=900)
