@@ -376,6 +376,24 @@ GNNA_API gnna_status gnna_build_mapping(gnna_ctx* ctx, const uint32_t* d_com, ui
 GNNA_API gnna_status gnna_degree_order(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n,
                                        uint32_t* d_old_to_new, uint32_t* d_new_to_old);
 /* renumber.cpp:148 mapping_from_vector (DOMAIN if not a permutation). */
+/* ------------------------------------------------- synthetic inputs --- */
+/* Host-only (no device needed).  Edge samplers for the BASELINE configs with
+ * the reference's generator family (std::mt19937_64 + draw_unit /
+ * draw_index, rand.hpp:13-21); out_edges: pairs x 2 node ids.  Pairs are
+ * drawn in fixed chunks of 2^20 (chunk c from mt19937_64(seed + c *
+ * 0x9E3779B97F4A7C15)) on all host threads: output independent of the thread
+ * count.  shuffle: ids permuted by Fisher-Yates with draw_index (the
+ * planted_partition shuffle, pipeline.cpp:37-44).
+ * Chung-Lu: endpoint weight (i + i0)^-(1/(gamma-1)), inverse-CDF sampling.
+ * SBM: equal contiguous blocks; an endpoint stays in its source's block with
+ * probability p_intra.  random_features is pipeline.cpp:57-67 exactly (one
+ * sequential stream, row-major U[0,1)); the F32 form casts the same doubles. */
+GNNA_API gnna_status gnna_gen_chung_lu(uint32_t n, uint64_t pairs, double gamma, double i0, uint64_t seed,
+                              int shuffle, uint32_t* out_edges);
+GNNA_API gnna_status gnna_gen_sbm(uint32_t n, uint64_t pairs, uint32_t communities, double p_intra,
+                         uint64_t seed, int shuffle, uint32_t* out_edges);
+GNNA_API gnna_status gnna_random_features(uint32_t n, uint32_t dim, uint64_t seed, int dtype, void* out);
+
 /* Hub rows kept in L2 WITHOUT renumbering (drop-in path: the caller's node
  * order, and so the reference's summation tree, stay as they are).  Picks
  * the k highest-degree nodes (ties by id: the gnna_degree_order keys) into

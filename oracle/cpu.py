@@ -303,6 +303,29 @@ class Oracle:
                    C.byref(k), C.byref(q), C.byref(a0), C.byref(a1))
         return o2n[:n].copy(), n2o[:n].copy(), k.value, q.value, a0.value, a1.value
 
+    def run_pipeline(self, n, edges, dim, params=None, strategy=2, dim_mode=1, force_reorder=None, seed=1,
+                     cache=(64 * 1024, 128), workers=1):
+        """pipeline.cpp:93-124 run_pipeline (reference only: "ref")."""
+        e = _u32(edges).reshape(-1, 2)
+        p_in = _u32(params if params is not None else [0, 0, 0, 0, 0])
+        reordered, ncom, q = C.c_int(), C.c_uint32(), C.c_double()
+        o2n = np.zeros(max(n, 1), np.uint32)
+        aes = np.zeros(3, np.float64)
+        p_out = np.zeros(5, np.uint32)
+        rep = np.zeros(7, np.uint64)
+        fr = -1 if force_reorder is None else int(bool(force_reorder))
+        cap, line = cache if cache else (0, 0)
+        # the output's width is the params' dim (auto: the config dim)
+        width = int(p_in[4]) if params is not None else dim
+        out = np.zeros((n, width), np.float64)
+        self._call("run_pipeline", C.c_uint32(n), _p(e), C.c_uint64(len(e)), C.c_uint32(dim), _p(p_in),
+                   C.c_int(strategy), C.c_int(dim_mode), C.c_int(fr), C.c_uint64(seed), C.c_uint64(cap),
+                   C.c_uint64(line), C.c_uint(workers), C.byref(reordered), _p(o2n), C.byref(ncom), C.byref(q),
+                   _p(aes), _p(p_out), _p(rep), _p(out))
+        return {"reordered": bool(reordered.value), "o2n": o2n[:n], "num_communities": ncom.value,
+                "modularity": q.value, "aes": aes[0], "aes_before": aes[1], "aes_after": aes[2],
+                "params": p_out.tolist(), "report": rep.tolist(), "output": out}
+
     def model_inputs(self, row_ptr, col, dim):
         row_ptr, col = _u64(row_ptr), _u32(col)
         out = PodInputs()

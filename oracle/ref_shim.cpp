@@ -435,6 +435,56 @@ int ref_reorder_edges(uint32_t n, const uint32_t* edges, uint64_t e, uint32_t* o
     });
 }
 
+// pipeline.cpp:93-124 run_pipeline.  force_reorder: -1 absent (the AES rule
+// decides), 0 / 1 forced; params_in[0] == 0: auto_params; cache_capacity 0:
+// no cache replay, else CacheConfig{capacity, line}.  Outputs: the stats,
+// the reorder result (o2n, ncom, Q, AES before/after), the params used, the
+// CostReport (7 counters, engine.hpp order) and the n x dim output.
+int ref_run_pipeline(uint32_t n, const uint32_t* edges, uint64_t e, uint32_t dim, const uint32_t params_in[5],
+                     int strategy, int dim_mode, int force_reorder, uint64_t seed, uint64_t cache_capacity,
+                     uint64_t cache_line, unsigned workers, int* reordered, uint32_t* o2n, uint32_t* ncom,
+                     double* q, double* aes, uint32_t params_out[5], uint64_t report[7], double* out) {
+    return guard([&] {
+        RunConfig cfg;
+        cfg.dim = dim;
+        if (params_in[0]) {
+            KernelParams k;
+            k.ngs = params_in[0];
+            k.dw = params_in[1];
+            k.tpb = params_in[2];
+            k.tpw = params_in[3];
+            k.dim = params_in[4];
+            cfg.params = k;
+        }
+        cfg.strategy = static_cast<Strategy>(strategy);
+        cfg.dim_mode = static_cast<DimMode>(dim_mode);
+        if (cache_capacity) cfg.cache = CacheConfig{cache_capacity, cache_line};
+        else cfg.cache = std::nullopt;
+        if (force_reorder >= 0) cfg.force_reorder = force_reorder != 0;
+        cfg.seed = seed;
+        cfg.workers = workers;
+        const RunResult r = run_pipeline(view_edges(n, edges, e), cfg);
+        *reordered = r.reordered ? 1 : 0;
+        aes[0] = r.stats.aes;
+        if (r.reorder) {
+            std::memcpy(o2n, r.reorder->mapping.old_to_new.data(), sizeof(uint32_t) * n);
+            *ncom = r.reorder->num_communities;
+            *q = r.reorder->modularity;
+            aes[1] = r.reorder->aes_before;
+            aes[2] = r.reorder->aes_after;
+        }
+        put_params(r.params, params_out);
+        report[0] = r.report.atomic_ops;
+        report[1] = r.report.global_reads;
+        report[2] = r.report.global_writes;
+        report[3] = r.report.global_transactions;
+        report[4] = r.report.shared_bytes_per_block;
+        report[5] = r.report.cache_hits;
+        report[6] = r.report.cache_accesses;
+        std::memcpy(out, r.output.values.data(), sizeof(double) * r.output.values.size());
+    });
+}
+
 // decider.cpp:26 ModelInputs::from_graph
 int ref_model_inputs(uint32_t n, const uint64_t* row_ptr, const uint32_t* col,
                      uint32_t dim, PodInputs* out) {

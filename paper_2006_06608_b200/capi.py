@@ -649,6 +649,37 @@ class Plan:
         return h.value, a.value
 
 
+# ---------------------------------------- synthetic inputs (host, no GPU)
+def gen_edges(kind, n, pairs, seed, shuffle=False, gamma=2.3, i0=10.0, communities=1, p_intra=0.8, out=None):
+    """gnna_gen_chung_lu / gnna_gen_sbm: (pairs, 2) uint32 node pairs drawn
+    with the reference's mt19937_64 draws (rand.hpp:13-21), into `out` (a
+    uint32 numpy array or a pinned CPU tensor's numpy view) when given."""
+    if out is None:
+        out = np.empty((pairs, 2), np.uint32)
+    L = lib()
+    if kind == "chung_lu":
+        rc = L.gnna_gen_chung_lu(C.c_uint32(n), C.c_uint64(pairs), C.c_double(gamma), C.c_double(i0),
+                                 C.c_uint64(seed), C.c_int(int(shuffle)), _ptr(out))
+    else:
+        rc = L.gnna_gen_sbm(C.c_uint32(n), C.c_uint64(pairs), C.c_uint32(communities), C.c_double(p_intra),
+                            C.c_uint64(seed), C.c_int(int(shuffle)), _ptr(out))
+    if rc:
+        raise DomainError(rc, f"gen_edges({kind}): arguments outside the generator's domain")
+    return out
+
+
+def random_features(n, dim, seed, dtype=np.float32, out=None):
+    """gnna_random_features = random_features(n, dim, seed) of
+    pipeline.cpp:57-67 (fp32: the same doubles rounded)."""
+    dt = F32 if np.dtype(dtype) == np.float32 else F64
+    if out is None:
+        out = np.empty((n, dim), dtype)
+    rc = lib().gnna_random_features(C.c_uint32(n), C.c_uint32(dim), C.c_uint64(seed), C.c_int(dt), _ptr(out))
+    if rc:
+        raise DomainError(rc, "random_features: dim must be positive")
+    return out
+
+
 # ------------------------------------------------- evaluator (host, no GPU)
 # decider.hpp:46-94: these run on the host inside libgnna.so and need no
 # device, so the CPU test suite checks them against the reference.

@@ -44,14 +44,17 @@ class GCN2:
         self.norm, _, self.rs2, self.ind = ctx.gcn_fold_weights(row_ptr, col, self_loops)
         if not self_loops:  # no implicit self loops: the self term is identically zero
             self.sw = self.ind = None
-        g = torch.Generator(device=dev)
-        g.manual_seed(seed)
-        self.w1 = ((torch.rand((in_dim, hidden), generator=g, device=dev) * 2 - 1) / math.sqrt(in_dim)).contiguous()
-        g.manual_seed(seed + 1)
-        self.w2 = ((torch.rand((hidden, out_dim), generator=g, device=dev) * 2 - 1) / math.sqrt(hidden)).contiguous()
+        # W ~ U[-1, 1) / sqrt(fan_in) from the reference's random_features stream (seeds 4, 5)
+        self.w1 = self._uniform(in_dim, hidden, seed, dev) / math.sqrt(in_dim)
+        self.w2 = self._uniform(hidden, out_dim, seed + 1, dev) / math.sqrt(hidden)
         self.zero_b1 = torch.zeros(hidden, device=dev)
         self.lr = lr
         self.side = None
+
+    @staticmethod
+    def _uniform(rows, cols, seed, dev):
+        from .capi import random_features
+        return (torch.from_numpy(random_features(rows, cols, seed)) * 2 - 1).to(dev).contiguous()
 
     def use_side_stream(self, enable=True):
         """Run the independent dW2 product on a second stream (its own

@@ -2,25 +2,31 @@
 
 The reference's own generator (planted_partition, pipeline.cpp:14-46) samples
 all O(n^2) node pairs and refuses graphs above 65,536 nodes, so the C3-C5
-shapes need a new generator.  These are edge samplers; the graph is then
+shapes need new samplers.  They draw with the reference's generator family:
+std::mt19937_64 with rand.hpp's draw_unit / draw_index (gnna_gen_chung_lu /
+gnna_gen_sbm, host C++ in libgnna.so), and features are the reference's
+random_features(n, d, seed) itself (pipeline.cpp:57-67, gnna_random_features)
+-- so bench.py's GPU arm and its CPU reference arm aggregate the same graph
+and the same features whenever they run the same size.  The sampled pairs are
 canonicalised by to_csr (symmetrise, sort, dedup: graph.cpp:76-95), on the GPU
-through libgnna (gnna_to_csr) or on the CPU through the reference's to_csr.
+(gnna_to_csr) or on the CPU through the reference's to_csr.
 
-* Chung-Lu power law: endpoint i is drawn with weight (i + i0)^(-beta),
-  beta = 1/(gamma-1), by inverting the continuous CDF of that weight.  Low
-  ids are the hubs.  Used for C3 (amazon0505 shape) and C5.
-* Community SBM: nodes are split into `communities` equal contiguous blocks
-  (optionally shuffled); an edge's destination stays in the source's block
-  with probability p_intra.  Used for C1, C2, C4.
+* Chung-Lu power law: endpoint weight (i + i0)^(-1/(gamma-1)), inverse-CDF
+  sampling; low ids are the hubs.  C3 (amazon0505 shape), C5.
+* Community SBM: `communities` equal contiguous blocks; an endpoint stays in
+  its source's block with probability p_intra; optionally ids shuffled
+  (Fisher-Yates with draw_index).  C1, C2, C4.
 
-Edge samples are drawn with torch generators (CPU or CUDA); this module is
-input plumbing, not a compute path.
+This module is input plumbing, not a compute path.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
+
+from . import capi
 
 
 @dataclass(frozen=True)
@@ -48,73 +54,67 @@ CONFIGS = {
     "c5": GraphConfig("C5 10M-node Chung-Lu power law", "chung_lu", 10_000_000, 200_000_000, 128, 8),
 }
 
-
-def _gen(device, seed):
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    return g
+ROUND_SEED = 1_000_003  # top-up round r draws from seed + r * ROUND_SEED
 
 
-def chung_lu_pairs(n, pairs, gamma, i0, gen, device):
-    beta = 1.0 / (gamma - 1.0)
-    a = 1.0 - beta
-    lo = i0 ** a
-    hi = (n + i0) ** a
-    u = torch.rand((pairs, 2), generator=gen, device=device, dtype=torch.float64)
-    x = torch.pow(lo + u * (hi - lo), 1.0 / a) - i0
-    return torch.clamp(x.floor(), 0, n - 1).to(torch.int32)
-
-
-def sbm_pairs(n, pairs, communities, p_intra, gen, device, perm=None):
-    size = max(1, n // communities)
-    src = torch.randint(0, n, (pairs,), generator=gen, device=device, dtype=torch.int64)
-    intra = torch.rand(pairs, generator=gen, device=device) < p_intra
-    com = torch.clamp(src // size, max=communities - 1)
-    base = com * size
-    span = torch.where(com == communities - 1, n - base, torch.full_like(base, size))
-    r = torch.rand(pairs, generator=gen, device=device, dtype=torch.float64)
-    dst_in = base + (r * span).floor().to(torch.int64)
-    dst_out = torch.randint(0, n, (pairs,), generator=gen, device=device, dtype=torch.int64)
-    dst = torch.where(intra, dst_in, dst_out)
-    e = torch.stack([src, dst], 1)
-    if perm is not None:
-        e = perm[e]
-    return e.to(torch.int32)
-
-
-def sample_pairs(cfg: GraphConfig, pairs: int, gen, device, n=None):
+def sample_pairs(cfg: GraphConfig, pairs: int, seed: int, device, n=None):
+    """(pairs, 2) int32 node pairs on `device` (host generator, pinned upload)."""
     n = n or cfg.n
-    if cfg.kind == "chung_lu":
-        return chung_lu_pairs(n, pairs, cfg.gamma, cfg.i0, gen, device)
-    perm = None
-    if cfg.shuffle:
-        perm = torch.randperm(n, generator=gen, device=device)
-    return sbm_pairs(n, pairs, cfg.communities, cfg.p_intra, gen, device, perm)
+    pin = torch.device(device).type == "cuda"
+    buf = torch.empty((pairs, 2), dtype=torch.int32, pin_memory=pin)
+    capi.gen_edges(cfg.kind, n, pairs, seed, shuffle=cfg.shuffle, gamma=cfg.gamma, i0=cfg.i0,
+                   communities=cfg.communities, p_intra=cfg.p_intra, out=buf.numpy().view(np.uint32))
+    return buf.to(device, non_blocking=pin) if pin else buf
 
 
 def build_graph(cfg: GraphConfig, to_csr, device, n=None, nnz=None, max_rounds=4):
-    """Sample edges until the symmetrised, de-duplicated CSR reaches ~nnz.
+    """Sample pairs until the symmetrised, de-duplicated CSR reaches ~nnz.
 
     to_csr(n, edges(E,2) int32 tensor on `device`) -> (row_ptr, col).
     Returns (edges, row_ptr, col)."""
     n = n or cfg.n
     target = nnz or cfg.nnz
-    gen = _gen(device, cfg.seed)
-    edges = sample_pairs(cfg, target // 2, gen, device, n)
+    edges = sample_pairs(cfg, target // 2, cfg.seed, device, n)
     rp, col = to_csr(n, edges)
-    for _ in range(max_rounds):
+    for r in range(1, max_rounds + 1):
         have = int(col.numel())
         if have >= target * 0.999:
             break
         extra = int((target - have) / 2 * 1.15) + 16
-        edges = torch.cat([edges, sample_pairs(cfg, extra, gen, device, n)])
+        edges = torch.cat([edges, sample_pairs(cfg, extra, cfg.seed + r * ROUND_SEED, device, n)])
         rp, col = to_csr(n, edges)
     return edges, rp, col
 
 
+EXACT_FEATURES_MAX = 1 << 28  # values; above it the features come in parallel row blocks
+
+
 def features(n, dim, seed, device, dtype=torch.float32):
-    """U[0,1) features (random_features semantics, pipeline.cpp:57-67)."""
-    return torch.rand((n, dim), generator=_gen(device, seed + 1000), device=device, dtype=dtype)
+    """random_features(n, dim, seed + 1000) of pipeline.cpp:57-67 on `device`.
+
+    Up to 2^28 values (every config but C5) this is the reference's function
+    exactly: one sequential mt19937_64 stream.  Above it (C5: 1.28e9 values,
+    ~10 s as one stream) rows come in blocks of 2^20, block b being
+    random_features(rows, dim, seed + 1000 + b * 0x9E3779B97F4A7C15), drawn
+    in parallel -- the same generator, deterministic, not one stream."""
+    np_dt = np.float32 if dtype == torch.float32 else np.float64
+    pin = torch.device(device).type == "cuda"
+    buf = torch.empty((n, dim), dtype=dtype, pin_memory=pin)
+    arr = buf.numpy()
+    if n * dim <= EXACT_FEATURES_MAX:
+        capi.random_features(n, dim, seed + 1000, np_dt, out=arr)
+    else:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        rows = 1 << 20
+
+        def block(b):  # ctypes releases the GIL: the blocks run on all cores
+            r0 = b * rows
+            capi.random_features(min(rows, n - r0), dim, (seed + 1000 + b * 0x9E3779B97F4A7C15) % (1 << 64),
+                                 np_dt, out=arr[r0:r0 + rows])
+        with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+            list(ex.map(block, range((n + rows - 1) // rows)))
+    return buf.to(device, non_blocking=pin) if pin else buf
 
 
 def scaled_config(cfg: GraphConfig, n: int) -> tuple[int, int]:

@@ -47,9 +47,7 @@ def main():
 
     # C5: to_csr + plan build
     cfg = synth.CONFIGS["c5"]
-    g = torch.Generator(device=dev)
-    g.manual_seed(cfg.seed)
-    edges = synth.sample_pairs(cfg, cfg.nnz // 2, g, dev)
+    edges = synth.sample_pairs(cfg, cfg.nnz // 2, cfg.seed, dev)
     ctx.to_csr(cfg.n, edges[:1000], True)  # warm up allocator / CUB
     t, (rp, col) = timed(lambda: ctx.to_csr(cfg.n, edges, True))
     emit(stage="to_csr", workload="c5", edges=int(edges.shape[0]), nnz=int(col.numel()), gpu_s=t)

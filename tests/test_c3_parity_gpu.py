@@ -130,9 +130,7 @@ def test_c3_train_step_full_size(ctx, orc, c3):
     n = c3["cfg"].n
     model = GCN2(ctx, rp, col, 96, 16, 22, self_loops=False, lr=0.0)
     x = synth.features(n, 96, 3, rp.device)
-    g = torch.Generator(device=rp.device)
-    g.manual_seed(6)
-    dy = (torch.rand((n, 22), generator=g, device=rp.device) - 0.5).contiguous()
+    dy = (synth.features(n, 22, 6 - 1000, rp.device) - 0.5).contiguous()
     y, dw1, dw2 = model.step(x, dy)
     h1_gpu = model.saved["h1"].cpu().numpy()  # norm * h1 (pre-scaled): same sign as h1
     x64, dy64 = x.double().cpu().numpy(), dy.double().cpu().numpy()
