@@ -259,7 +259,8 @@ def cpu_sample(cfg, n_nodes, seed_offset=0, order="natural"):
         rp, col2 = ref.to_csr(n, o2n[e], True)
         col = torch.from_numpy(col2.view(np.int32))
     col = col.numpy().view(np.uint32)
-    x = np.random.default_rng(cfg.seed + seed_offset).random((n, cfg.dim))
+    # the features both arms use: random_features(n, d, seed + 1000) (pipeline.cpp:57-67)
+    x = synth.features(n, cfg.dim, cfg.seed + seed_offset, "cpu", dtype=torch.float64).numpy()
     return ref, rp, col, x
 
 
@@ -519,6 +520,8 @@ def extra_workloads(ctx, dev, args, reps=10):
                     "effective_frac_of_measured_hbm": balg / t / 1e9 / peak, "l2": "flushed between calls",
                     "parity": rel_check(got, want, bound)})
     out.append(train_step(ctx, dev, scratch, reps))
+    for w in ("c3", "c4"):
+        out.append(dropin_f64(w))
     # traffic of one call of every case, measured by an ncu child of this run
     # (cache flushed before each launch, like the timed calls)
     if not args.no_ncu:
@@ -536,6 +539,51 @@ def extra_workloads(ctx, dev, args, reps=10):
             tr["source"] = "this run: ncu --metrics child (bench.py --probe extras), cache flushed per launch"
             e["traffic"] = tr
     return out
+
+
+def dropin_f64(workload, reps=5):
+    """The drop-in at the reference's own precision: a C++ caller
+    (tests/cpp/bin/dropin_check config) of gnnsim::aggregate_scheduled with
+    a host FeatureMatrix of doubles -- upload, cached plan, fp64 K3 (bitwise
+    the reference's tree), download -- against the reference's own
+    aggregate_scheduled (oracle/_ref, all host threads) on the SAME graph
+    (synth's samplers), features (random_features) and parameters (the
+    reference's auto_params).  Wall-clock per warm call, both arms."""
+    import torch
+    from oracle.cpu import Oracle
+    from paper_2006_06608_b200 import synth
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", "dropin_check")
+    if not os.path.exists(exe):
+        return {"case": f"{workload}/dropin_f64", "unavailable": "tests/cpp/bin/dropin_check not built"}
+    r = subprocess.run([exe, "config", workload, str(reps)], capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"case": f"{workload}/dropin_f64", "unavailable": (r.stderr or r.stdout)[-300:]}
+    ours = json.loads(r.stdout.strip().splitlines()[-1])
+    ref = Oracle("ref")
+    cfg = synth.CONFIGS[workload]
+
+    def to_csr(n, e):
+        rp, col = ref.to_csr(n, e.numpy().astype(np.uint32), True)
+        return rp, torch.from_numpy(col.view(np.int32))
+    _, rp, col = synth.build_graph(cfg, to_csr, "cpu")
+    col = col.numpy().view(np.uint32)
+    h = 1469598103934665603
+    for v in np.asarray(rp, np.uint64).tolist():
+        h = ((h ^ v) * 1099511628211) % (1 << 64)
+    x = synth.features(cfg.n, cfg.dim, cfg.seed, "cpu", dtype=torch.float64).numpy()
+    params = [int(v) for v in ref.auto_params(ref.model_inputs(rp, col, cfg.dim))]
+    workers = os.cpu_count() or 1
+    time_reference(ref, rp, col, x, params, workers, 1)
+    t_ref = time_reference(ref, rp, col, x, params, workers, 3)
+    return {"case": f"{workload}/dropin_f64", "workload": cfg.name, "dtype": "f64",
+            "path": "gnnsim::aggregate_scheduled (libgnnsim_b200.so, host FeatureMatrix) from a C++ caller",
+            "n": ours["n"], "nnz": ours["nnz"], "dim": cfg.dim, "params": ours["params"],
+            "dropin_ms_per_call": ours["warm_call_ms_median"], "dropin_first_call_ms": ours["first_call_ms"],
+            "reference_ms_per_call": t_ref * 1e3, "reference_workers": workers,
+            "speedup_vs_reference": t_ref * 1e3 / ours["warm_call_ms_median"],
+            "same_graph": ours["row_ptr_fnv"] == f"{h:016x}" and ours["nnz"] == len(col),
+            "same_params": ours["params"] == params[:3], "cache_hit": ours["cache_hit"],
+            "reference": "oracle/_ref aggregate_scheduled (WarpShared, Cyclic, no cache replay), same x"}
 
 
 def probe_extras(ctx, dev, args):

@@ -6,6 +6,11 @@
 //   dropin_check bench N E D R  timing: a shuffled power-law graph of N nodes
 //                               and ~E undirected edges, D-wide features, R
 //                               timed calls with the hub layout on and off
+//   dropin_check config C R     timing on BASELINE config C (c1..c5): the same
+//                               graph as paper_2006_06608_b200/synth.py (the
+//                               gnna_gen_* samplers, same seeds and top-up
+//                               rounds) and random_features(n, d, seed+1000),
+//                               the reference's auto_params; R warm calls
 //
 // Graphs: Chung-Lu sampling with the reference's own draws (mt19937_64 +
 // draw_unit / draw_index, rand.hpp) and a Fisher-Yates id shuffle, so the
@@ -18,9 +23,11 @@
 #include <cstring>
 #include <numeric>
 #include <random>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "gnna.h"
 #include "gnnsim/gnnsim_b200.hpp"
 
 using namespace gnnsim;
@@ -172,12 +179,90 @@ static int bench(std::uint32_t n, std::uint64_t pairs, std::uint32_t dim, int re
     return 0;
 }
 
+struct Config {
+    const char* kind;
+    std::uint32_t n;
+    std::uint64_t nnz;
+    std::uint32_t dim;
+    std::uint64_t seed;
+    std::uint32_t communities;
+    double p_intra;
+    bool shuffle;
+};
+
+// synth.py CONFIGS
+static bool config_of(const std::string& name, Config& c) {
+    if (name == "c1") c = {"sbm", 2708, 10556, 16, 1, 7, 0.8, false};
+    else if (name == "c2") c = {"sbm", 19717, 88648, 64, 2, 3, 0.8, true};
+    else if (name == "c3") c = {"chung_lu", 410236, 4878874, 16, 3, 1, 0.8, false};
+    else if (name == "c4") c = {"sbm", 88784, 2093194, 64, 7, 39, 0.9, false};
+    else if (name == "c5") c = {"chung_lu", 10000000, 200000000, 128, 8, 1, 0.8, false};
+    else return false;
+    return true;
+}
+
+static void sample(const Config& c, std::uint64_t pairs, std::uint64_t seed, EdgeList& el) {
+    std::vector<std::uint32_t> e(2 * pairs);
+    const gnna_status st = std::strcmp(c.kind, "sbm") == 0
+                               ? gnna_gen_sbm(c.n, pairs, c.communities, c.p_intra, seed, c.shuffle, e.data())
+                               : gnna_gen_chung_lu(c.n, pairs, 2.3, 10.0, seed, c.shuffle, e.data());
+    if (st != GNNA_OK) throw std::runtime_error("generator");
+    for (std::uint64_t i = 0; i < pairs; ++i) el.edges.emplace_back(e[2 * i], e[2 * i + 1]);
+}
+
+// synth.build_graph: sample nnz/2 pairs, top up (seed + r * 1000003) until ~nnz
+static CsrGraph config_graph(const Config& c) {
+    EdgeList el;
+    el.num_nodes = c.n;
+    sample(c, c.nnz / 2, c.seed, el);
+    CsrGraph g = to_csr(el, true);
+    for (int r = 1; r <= 4; ++r) {
+        const std::uint64_t have = g.col_idx.size();
+        if (static_cast<double>(have) >= c.nnz * 0.999) break;
+        const auto extra = static_cast<std::uint64_t>((static_cast<double>(c.nnz) - have) / 2 * 1.15) + 16;
+        sample(c, extra, c.seed + r * 1000003ull, el);
+        g = to_csr(el, true);
+    }
+    return g;
+}
+
+static int config_bench(const std::string& name, int reps) {
+    Config c;
+    if (!config_of(name, c)) return 2;
+    auto t0 = std::chrono::steady_clock::now();
+    const CsrGraph g = config_graph(c);
+    const FeatureMatrix x = random_features(c.n, c.dim, c.seed + 1000);
+    const double gen_ms = ms_since(t0);
+    const KernelParams p = auto_params(ModelInputs::from_graph(g, c.dim));  // decider.cpp, as a user would
+    EngineOptions opt;
+    opt.cache = std::nullopt;  // the aggregation alone (the LRU replay is its own cost model)
+    std::uint64_t h = 1469598103934665603ull;
+    for (const auto v : g.row_ptr) h = (h ^ v) * 1099511628211ull;
+    std::vector<double> ms;
+    b200::CallStats st{};
+    for (int r = 0; r < reps + 1; ++r) {
+        t0 = std::chrono::steady_clock::now();
+        auto res = aggregate_scheduled(g, x, p, Strategy::WarpShared, DimMode::Cyclic, opt);
+        ms.push_back(ms_since(t0));
+        st = b200::last_call_stats();
+    }
+    std::vector<double> warm(ms.begin() + 1, ms.end());
+    std::sort(warm.begin(), warm.end());
+    std::printf("{\"config\": \"%s\", \"n\": %u, \"nnz\": %zu, \"dim\": %u, \"row_ptr_fnv\": \"%016llx\", "
+                "\"params\": [%u, %u, %u], \"generate_ms\": %.1f, \"first_call_ms\": %.3f, "
+                "\"warm_call_ms_median\": %.3f, \"warm_calls\": %d, \"cache_hit\": %s, \"hub_rows\": %u}\n",
+                name.c_str(), c.n, g.col_idx.size(), c.dim, (unsigned long long)h, p.ngs, p.dw, p.tpb, gen_ms, ms[0],
+                warm[warm.size() / 2], reps, st.cache_hit ? "true" : "false", st.hub_rows);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "check";
     if (mode == "check") return check();
+    if (mode == "config" && argc >= 4) return config_bench(argv[2], std::atoi(argv[3]));
     if (mode == "bench" && argc >= 6)
         return bench(std::strtoul(argv[2], nullptr, 10), std::strtoull(argv[3], nullptr, 10),
                      std::strtoul(argv[4], nullptr, 10), std::atoi(argv[5]));
-    std::fprintf(stderr, "usage: dropin_check check | bench N PAIRS DIM REPS\n");
+    std::fprintf(stderr, "usage: dropin_check check | bench N PAIRS DIM REPS | config c1..c5 REPS\n");
     return 2;
 }
