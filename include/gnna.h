@@ -453,6 +453,15 @@ GNNA_API gnna_status gnna_b200_profile(gnna_ctx* ctx, gnna_model_inputs* in);
  * with G = n + nnz/ngs (c_unit 24 ps, c_edge 95 ns, c_ramp 0.46, fitted on
  * measured K3 sweeps); tpb = 512; dw = select_dw(dim).  hbm_gbs <= 0 uses
  * 6553 (MEASURED_PEAKS.json).  *est_us (may be NULL) = the model's K3 time. */
+/* The B200 evaluator on a device graph: reads the degree profile (max
+ * degree; the gather share of the highest-degree rows that fit in half the
+ * L2 and in a 48 MB window) and the device's SM count and L2 size, and
+ * returns the parameters (ngs; tpb 512; dw = select_dw), the model's K3
+ * estimate (us) and the recommended L2 window for the hub rows (0: none).
+ * hbm_gbs <= 0: the B200's measured 6,544.7 GB/s.  dtype: element size. */
+GNNA_API gnna_status gnna_b200_plan_params(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n, uint32_t dim,
+                                  int dtype, double hbm_gbs, gnna_params* out, double* est_us,
+                                  uint64_t* l2_window_bytes);
 GNNA_API gnna_status gnna_b200_auto_params(const gnna_model_inputs* in, uint64_t max_degree, double hbm_gbs,
                                   gnna_params* out, double* est_us);
 /* Measured-latency tuner: times gnna_aggregate (F32) on the live graph for

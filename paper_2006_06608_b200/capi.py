@@ -527,23 +527,25 @@ class Context:
         return best, ms.value
 
     # ------------------------------------------------------------- decider
-    def b200_params(self, row_ptr, dim, hbm_gbs=0.0):
-        """The B200 evaluator (gnna_b200_auto_params) on this graph: (Params, model K3 microseconds)."""
-        mi = self.model_inputs(row_ptr, dim, b200=True)
-        _, maxd, _ = self.degree_stats(row_ptr)
+    def b200_params(self, row_ptr, dim, hbm_gbs=0.0, dtype=None, window=False):
+        """The B200 evaluator (gnna_b200_plan_params) on this device graph:
+        (Params, model K3 microseconds), plus the recommended L2 window bytes
+        for the hub rows when window=True.  dtype: torch.float32 (default) or
+        torch.float64 (element size of the features)."""
         if not hbm_gbs:
             try:
                 import json
                 hbm_gbs = float(json.load(open(os.path.join(os.path.dirname(HERE), "MEASURED_PEAKS.json")))["hbm_gbs"])
             except Exception:
                 hbm_gbs = 0.0
+        dt = F64 if dtype is not None and dtype == self.torch.float64 else F32
         p = Params()
         est = C.c_double()
-        rc = self.L.gnna_b200_auto_params(C.byref(mi), C.c_uint64(maxd), C.c_double(hbm_gbs), C.byref(p),
-                                          C.byref(est))
-        if rc:
-            raise DomainError(rc, self.L.gnna_decider_last_error().decode())
-        return p, est.value
+        win = C.c_uint64()
+        self._check(self.L.gnna_b200_plan_params(self.h, _ptr(row_ptr), C.c_uint32(row_ptr.numel() - 1),
+                                                 C.c_uint32(dim), C.c_int(dt), C.c_double(hbm_gbs), C.byref(p),
+                                                 C.byref(est), C.byref(win)))
+        return (p, est.value, win.value) if window else (p, est.value)
 
     def auto_params(self, inputs: ModelInputs) -> Params:
         p = Params()

@@ -38,4 +38,19 @@ struct Domain {
     const char* msg;
 };
 
+// B200 evaluator inputs: the graph's profile and the device's properties.
+struct B200Inputs {
+    uint64_t num_nodes = 0, num_edges = 0;
+    uint32_t dim = 0, elem = 4;        // row width and element bytes (fp32 / fp64)
+    uint64_t max_degree = 0;
+    double l2_hit_share = 0.0;         // gather share of the top-degree rows that fit in L2/2 (x > L2)
+    uint64_t window_bytes = 0;         // candidate L2 window (hub rows)
+    double window_share = 0.0;         // gather share of the rows that fit in the window
+    double window_rows_frac = 0.0;     // those rows / n
+    uint32_t num_sms = 148;
+    uint64_t l2_bytes = 0;
+    double hbm_gbs = 0.0;
+};
+gnna_params b200_params(const B200Inputs& g, double* est_us, uint64_t* window_bytes);
+
 }  // namespace gnna_decider

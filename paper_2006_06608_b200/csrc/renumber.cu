@@ -13,6 +13,7 @@
 #include <cub/device/device_select.cuh>
 
 #include "gnna_common.cuh"
+#include "host/decider_core.hpp"
 
 namespace gnna {
 uint64_t csr_from_keys(gnna_ctx* ctx, uint64_t* keys, uint64_t m, uint32_t n, uint64_t* row_ptr, uint32_t* col,
@@ -190,6 +191,15 @@ __global__ void k7_gather_rows(const T* __restrict__ x, uint32_t dim, const uint
         const uint64_t r = i / dim, c = i - r * dim;
         out[i] = x[(uint64_t)rows[r] * dim + c];
     }
+}
+
+// Sum of the k largest degrees from the sorted (~deg << 32 | id) keys.
+__global__ void k7_topk_degree_sum(const uint64_t* __restrict__ keys, uint64_t k, unsigned long long* __restrict__ out) {
+    unsigned long long s = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += (uint64_t)gridDim.x * blockDim.x)
+        s += (uint32_t)~(uint32_t)(keys[i] >> 32);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
 }  // namespace
@@ -392,6 +402,54 @@ gnna_status gnna_gather_rows(gnna_ctx* ctx, int dtype, const void* d_x, uint32_t
             k7_gather_rows<double><<<gnna::grid_for(total, 256), 256, 0, ctx->stream>>>(
                 static_cast<const double*>(d_x), dim, d_rows, count, static_cast<double*>(d_out));
         gnna::launched(ctx, "k7_gather_rows");
+    });
+}
+
+gnna_status gnna_b200_plan_params(gnna_ctx* ctx, const uint64_t* d_row_ptr, uint32_t n, uint32_t dim, int dtype,
+                                  double hbm_gbs, gnna_params* out, double* est_us, uint64_t* l2_window_bytes) {
+    return gnna::guard(ctx, [&] {
+        gnna::require_ctx(ctx);
+        if (!out) gnna::raise(GNNA_ERR_DOMAIN, "b200_plan_params: null output");
+        if (dtype != GNNA_F32 && dtype != GNNA_F64) gnna::raise(GNNA_ERR_DOMAIN, "unknown dtype");
+        if (dim == 0) gnna::raise(GNNA_ERR_DOMAIN, "dim must be positive");
+        cudaStream_t s = ctx->stream;
+        gnna_decider::B200Inputs g{};
+        g.num_nodes = n;
+        g.dim = dim;
+        g.elem = dtype == GNNA_F32 ? 4 : 8;
+        g.num_sms = (uint32_t)ctx->num_sms;
+        g.l2_bytes = ctx->l2_bytes > 0 ? (uint64_t)ctx->l2_bytes : 0;
+        g.hbm_gbs = hbm_gbs;
+        const uint64_t row = (uint64_t)dim * g.elem, l2 = g.l2_bytes ? g.l2_bytes : 126500000ull;
+        g.window_bytes = 48ull << 20;
+        if (n) {
+            gnna::to_host(ctx, &g.num_edges, d_row_ptr + n, 1);
+            DevBuf<uint64_t> keys(n, s);
+            k7_degree_keys<<<gnna::grid_for(n, 256), 256, 0, s>>>(d_row_ptr, n, keys.get());
+            gnna::launched(ctx, "k7_degree_keys");
+            gnna::sort_keys_u64(ctx, keys.get(), n, 64);
+            uint64_t k0 = 0;
+            gnna::to_host(ctx, &k0, keys.get(), 1);
+            g.max_degree = (uint32_t)~(uint32_t)(k0 >> 32);
+            // gather shares (symmetric CSR: in-degree = degree) of the rows that fit in L2/2 and in the window
+            const uint64_t kl2 = std::min<uint64_t>(n, l2 / 2 / row), kw = std::min<uint64_t>(n, g.window_bytes / row);
+            DevBuf<unsigned long long> sums(2, s);
+            GNNA_CUDA(cudaMemsetAsync(sums.get(), 0, 16, s));
+            if (kl2) k7_topk_degree_sum<<<gnna::grid_for(kl2, 256), 256, 0, s>>>(keys.get(), kl2, sums.get());
+            if (kw) k7_topk_degree_sum<<<gnna::grid_for(kw, 256), 256, 0, s>>>(keys.get(), kw, sums.get() + 1);
+            gnna::launched(ctx, "k7_topk_degree_sum");
+            unsigned long long h[2] = {0, 0};
+            gnna::to_host(ctx, h, sums.get(), 2);
+            const double nnz = g.num_edges ? (double)g.num_edges : 1.0;
+            g.l2_hit_share = h[0] / nnz;
+            g.window_share = h[1] / nnz;
+            g.window_rows_frac = (double)kw / n;
+        }
+        try {
+            *out = gnna_decider::b200_params(g, est_us, l2_window_bytes);
+        } catch (const gnna_decider::Domain& d) {
+            gnna::raise(GNNA_ERR_DOMAIN, d.msg);
+        }
     });
 }
 
