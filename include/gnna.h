@@ -186,7 +186,10 @@ GNNA_API gnna_status gnna_aggregate_ex(gnna_ctx* ctx, const gnna_plan* plan, int
  *     replica of y (multimem.st; the switch writes all copies, this rank's
  *     included, and d_y is not written separately).
  * The caller orders the peers' reads after every rank's kernel (a stream-
- * ordered cross-rank barrier).  Rows outside the plan are never written. */
+ * ordered cross-rank barrier), and this rank's stores after the peers'
+ * reads of the previous contents.  Rows outside the plan are never written.
+ * Node weights (opts->node_weight: GCN's gathered norm[u]) are supported on
+ * fp32 rows of at most one 16-byte chunk per lane (d <= 128). */
 #define GNNA_MAX_PEERS 7
 GNNA_API gnna_status gnna_aggregate_fanout(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
                                            const void* d_x, void* d_y, const gnna_agg_opts* opts,

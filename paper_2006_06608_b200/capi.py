@@ -614,22 +614,23 @@ class Plan:
                                                      _ptr(x), _ptr(out), C.byref(o)))
         return out
 
-    def aggregate_fanout(self, x, out, peers=(), mc=None, self_weight=None, alpha=0.0, row_scale=None, relu=False,
-                         mask=None, dim_mode=DIM_CYCLIC):
+    def aggregate_fanout(self, x, out, peers=(), mc=None, node_weight=None, self_weight=None, alpha=0.0,
+                         row_scale=None, relu=False, mask=None, dim_mode=DIM_CYCLIC):
         """gnna_aggregate_fanout: aggregate_ex on this plan's rows, every final
         row also written into each peer replica (device pointers or tensors:
         the other ranks' y, P2P-mapped) or, with `mc`, only through the NVLS
         multicast address of the replicated y."""
         self._feat(x, out)
         f32 = self.ctx.torch.float32
-        for t, nm in ((self_weight, "self_weight"), (row_scale, "row_scale")):
+        for t, nm in ((node_weight, "node_weight"), (self_weight, "self_weight"), (row_scale, "row_scale")):
             _dev(t, nm, f32, (self.n,))
         _dev(mask, "mask", x.dtype, tuple(x.shape))
         peers = [p if isinstance(p, int) else p.data_ptr() for p in peers]
         if len(peers) > 7:
             raise ValueError("at most 7 peer replicas (GNNA_MAX_PEERS)")
         arr = (C.c_void_p * max(1, len(peers)))(*peers)
-        o = AggOpts(int(x.shape[1]), None, _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu), _ptr(mask))
+        o = AggOpts(int(x.shape[1]), _ptr(node_weight), _ptr(self_weight), float(alpha), _ptr(row_scale), int(relu),
+                    _ptr(mask))
         mcp = None if mc is None else (mc if isinstance(mc, int) else mc.data_ptr())
         self.ctx._check(self.ctx.L.gnna_aggregate_fanout(self.ctx.h, self.h, C.c_int(_dtype_code(x)),
                                                          C.c_int(dim_mode), _ptr(x), _ptr(out), C.byref(o), arr,

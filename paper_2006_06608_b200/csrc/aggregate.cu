@@ -764,7 +764,8 @@ template <class T, int VEC, int TEAM>
 void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, const gnna_plan* plan) {
     const bool fan = a.npeer || a.mc;
     constexpr bool kEW = std::is_same<T, float>::value;  // weighted gathers: fp32 path only
-    if (fan && a.nw) gnna::raise(GNNA_ERR_DOMAIN, "aggregate_fanout: node weights are not supported");
+    if (fan && a.nw && (!kEW || kmax != 1))
+        gnna::raise(GNNA_ERR_DOMAIN, "aggregate_fanout: node weights need fp32 rows of one chunk per lane");
     // split-node carries are combined by their last writer, zero-degree rows by
     // trailing blocks: one launch per aggregation
     a.unit_blocks = grid;
@@ -791,7 +792,9 @@ void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, con
     if (!total) return;
     if (total > 0x7fffffffull) gnna::raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
     const unsigned g = (unsigned)total;
-    if (fan) {  // fused all-gather: fp32 and fp64, unweighted gathers
+    if (fan && a.nw) {  // fused all-gather of a per-source-weighted gather (GCN's norm[u]), fp32
+        k3_aggregate<T, VEC, TEAM, 1, kEW, true><<<g, threads, smem, ctx->stream>>>(a);
+    } else if (fan) {  // fused all-gather: fp32 and fp64, unweighted gathers
         if (kmax == 1)
             k3_aggregate<T, VEC, TEAM, 1, false, true><<<g, threads, smem, ctx->stream>>>(a);
         else if (kmax == 2)

@@ -68,3 +68,24 @@ def test_fanout_epilogues_and_limits(ctx, orc):
         plan.aggregate_fanout(x, y, peers=[torch.zeros_like(y) for _ in range(8)])
     with pytest.raises(DomainError):
         plan.aggregate_fanout(x, y, peers=[0])  # null replica
+
+
+def test_fanout_with_node_weights(ctx, orc):
+    """The GCN gather (per-source norm[u], self weight, row scale) fused with
+    the all-gather: every replica gets the plain weighted K3's bits."""
+    from paper_2006_06608_b200.capi import Params
+    rng = np.random.default_rng(12)
+    n = 4000
+    rp, col = powerlaw(orc, rng, n, 12 * n)
+    drp, dcol = to_dev(rp, col)
+    for dim, r0, r1 in ((16, 0, 2100), (64, 700, 4000), (128, 1, 3999)):
+        plan = ctx.plan(drp, dcol, Params.make(ngs=16, dw=32, tpb=512, dim=dim), rows=(r0, r1))
+        x = torch.tensor(rng.random((n, dim)), dtype=torch.float32, device="cuda")
+        rs, sw, _ = ctx.gcn_weights(drp, dcol, True, edge_weights=False)
+        want = torch.zeros((n, dim), device="cuda")
+        plan.aggregate_ex(x, out=want, node_weight=rs, self_weight=sw, row_scale=rs)
+        y = torch.zeros((n, dim), device="cuda")
+        peers = [torch.zeros((n, dim), device="cuda") for _ in range(2)]
+        plan.aggregate_fanout(x, y, peers=peers, node_weight=rs, self_weight=sw, row_scale=rs)
+        for buf in [y] + peers:
+            assert torch.equal(buf[r0:r1], want[r0:r1]), dim
