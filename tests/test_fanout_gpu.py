@@ -79,7 +79,7 @@ def test_fanout_with_node_weights(ctx, orc):
     rp, col = powerlaw(orc, rng, n, 12 * n)
     drp, dcol = to_dev(rp, col)
     for dim, r0, r1 in ((16, 0, 2100), (64, 700, 4000), (128, 1, 3999)):
-        plan = ctx.plan(drp, dcol, Params.make(ngs=16, dw=32, tpb=512, dim=dim), rows=(r0, r1))
+        plan = ctx.plan(drp, dcol, Params.make(ngs=16, dw=32, tpb=256, dim=dim), rows=(r0, r1))
         x = torch.tensor(rng.random((n, dim)), dtype=torch.float32, device="cuda")
         rs, sw, _ = ctx.gcn_weights(drp, dcol, True, edge_weights=False)
         want = torch.zeros((n, dim), device="cuda")
@@ -89,3 +89,9 @@ def test_fanout_with_node_weights(ctx, orc):
         plan.aggregate_fanout(x, y, peers=peers, node_weight=rs, self_weight=sw, row_scale=rs)
         for buf in [y] + peers:
             assert torch.equal(buf[r0:r1], want[r0:r1]), dim
+    # rows wider than one chunk per lane (tpb 512 caps teams at 16 lanes: d 128 is two chunks) are refused
+    from paper_2006_06608_b200.capi import DomainError
+    plan = ctx.plan(drp, dcol, Params.make(ngs=16, dw=32, tpb=512, dim=128))
+    x = torch.rand((n, 128), device="cuda")
+    with pytest.raises(DomainError):
+        plan.aggregate_fanout(x, torch.zeros_like(x), peers=[torch.zeros_like(x)], node_weight=rs)
