@@ -194,7 +194,8 @@ Hubs make_hubs(const std::uint64_t* rp, const std::uint32_t* col, std::uint32_t 
     h.dim = dim;
     const std::uint64_t row = std::uint64_t(dim) * sizeof(double);
     if (env_off("GNNSIM_HUB") || n == 0 || nnz == 0 || std::uint64_t(n) * row <= kHubMinBytes) return h;
-    const auto k = static_cast<std::uint32_t>(std::min<std::uint64_t>(n, kHubWindow / row));
+    auto k = static_cast<std::uint32_t>(std::min<std::uint64_t>(n, kHubWindow / row));
+    if (const char* e = std::getenv("GNNSIM_HUB_ROWS")) k = static_cast<std::uint32_t>(std::min<std::uint64_t>(n, std::strtoull(e, nullptr, 10)));
     Dev<std::uint32_t> list(k), col2(nnz);
     std::uint64_t edges = 0;
     ok(gnna_hub_remap(ctx(), rp, col, n, k, list.get(), col2.get(), &edges));
@@ -234,7 +235,8 @@ void aggregate_with_hubs(const gnna_plan* plan, const Hubs& hubs, std::uint32_t 
     }
     const double* tail = ext + std::size_t(n) * dim;
     std::uint64_t applied = 0;
-    ok(gnna_set_l2_window(ctx(), tail, std::uint64_t(hubs.k) * dim * sizeof(double), 1.0, &applied));
+    const std::uint64_t win = std::min<std::uint64_t>(std::uint64_t(hubs.k) * dim * sizeof(double), kHubWindow);
+    ok(gnna_set_l2_window(ctx(), tail, win, 1.0, &applied));
     const gnna_status st = gnna_aggregate(ctx(), plan, GNNA_F64, mode, ext, dy);
     gnna_set_l2_window(ctx(), nullptr, 0, 0.0, nullptr);
     ok(st);
