@@ -820,24 +820,30 @@ __global__ void __launch_bounds__(256) k6_gemm_tn_small(const float* __restrict_
 // one coalesced float4 per thread.  dW: TI x TJ = 4 x 4 register tiles over
 // row groups, summed in group order at the end.
 #ifndef GNNA_DB_ROWS
-#define GNNA_DB_ROWS 128
+#define GNNA_DB_ROWS 64
 #endif
 #ifndef GNNA_DB_STAGES
-#define GNNA_DB_STAGES 3
+#define GNNA_DB_STAGES 4
 #endif
 constexpr int DB_ROWS = GNNA_DB_ROWS, DB_STAGES = GNNA_DB_STAGES, DB_P = 32, DB_Q = 32;
 
 // Compile-time widths (P, Q <= 32): every inner loop unrolls, operands are
 // read as 16-/8-byte shared vectors and the FMA chains are independent.
+// Warp roles: warps 0-3 compute dz (one row half per thread per tile), warps
+// 4-7 accumulate dW (their 4x8 register tiles stay live only on that side,
+// so the kernel's register count is the larger role's, not the sum: 4 CTAs
+// of 256 threads per SM).  Both roles run the same tile loop and meet at
+// the same CTA barriers; all 256 threads issue the cp.async ring.
 template <int P, int Q>
-__global__ void __launch_bounds__(256) k6_dense_bwd(const float* __restrict__ dy, const float* __restrict__ w,
+__global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__ dy, const float* __restrict__ w,
                                                     const float* __restrict__ z, const double* __restrict__ row_scale,
                                                     uint32_t m, uint32_t rows_per_cta, float* __restrict__ dz,
                                                     float* __restrict__ part) {
     static_assert(P % 4 == 0 && Q % 2 == 0 && P <= DB_P && Q <= DB_Q, "dense_bwd widths");
     constexpr int TI = 4, TJ = 8;                       // dW register tile
-    constexpr int TQ = (Q + TJ - 1) / TJ, TILES = (P / TI) * TQ, RG = 256 / TILES;
+    constexpr int TQ = (Q + TJ - 1) / TJ, TILES = (P / TI) * TQ, RG = 128 / TILES;
     constexpr int PH = P / 2;                           // dz: 2 threads per row, PH outputs each
+    static_assert(2 * DB_ROWS % 128 == 0 && RG >= 1, "dense_bwd tiling");
     extern __shared__ __align__(16) float sm[];
     float* sdy = sm;                                    // [S][DB_ROWS * Q]
     float* sz = sdy + DB_STAGES * DB_ROWS * Q;          // [S][DB_ROWS * P]
@@ -848,9 +854,6 @@ __global__ void __launch_bounds__(256) k6_dense_bwd(const float* __restrict__ dy
         const uint32_t k = e / P, i = e % P;
         swt[e] = __ldg(w + (size_t)i * Q + k);
     }
-    const uint32_t grp = t / TILES, tile = t % TILES;
-    const bool active = grp < RG;
-    const uint32_t ti = (tile / TQ) * TI, tj = (tile % TQ) * TJ;
     const uint64_t r_begin = (uint64_t)blockIdx.x * rows_per_cta;
     const uint64_t r_end = r_begin + rows_per_cta < m ? r_begin + rows_per_cta : m;
     const uint32_t nblk = r_end > r_begin ? (uint32_t)((r_end - r_begin + DB_ROWS - 1) / DB_ROWS) : 0u;
@@ -885,53 +888,71 @@ __global__ void __launch_bounds__(256) k6_dense_bwd(const float* __restrict__ dy
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    float acc[TI][TJ];
+    // the tile loop both roles run: wait for tile blk, work(blk), free its slot
+    auto pipeline = [&](auto&& work) {
 #pragma unroll
-    for (int i = 0; i < TI; ++i)
-#pragma unroll
-        for (int j = 0; j < TJ; ++j) acc[i][j] = 0.f;
-#pragma unroll
-    for (int s = 0; s < DB_STAGES - 1; ++s) load(s);
-    for (uint32_t blk = 0; blk < nblk; ++blk) {
-        load(blk + DB_STAGES - 1);  // refills the slot freed at the end of the previous iteration
-        asm volatile("cp.async.wait_group %0;" ::"n"(DB_STAGES - 1) : "memory");
-        __syncthreads();
-        const uint32_t buf = blk % DB_STAGES;
-        const uint64_t r0 = r_begin + (uint64_t)blk * DB_ROWS;
-        const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)DB_ROWS ? r_end - r0 : (uint64_t)DB_ROWS);
-        const float* xdy = sdy + (size_t)buf * DB_ROWS * Q;
-        const float* xz = sz + (size_t)buf * DB_ROWS * P;
-        // dz = row_scale * (dy W^T): 2 threads per row, PH outputs each
-        for (uint32_t it = t; it < 2 * DB_ROWS; it += blockDim.x) {
-            const uint32_t dr = it / 2, half = it % 2;
-            if (dr >= nr) break;
-            float yv[Q];
-#pragma unroll
-            for (int k = 0; k < Q; k += 2) {
-                const float2 y2 = *reinterpret_cast<const float2*>(xdy + dr * Q + k);
-                yv[k] = y2.x;
-                yv[k + 1] = y2.y;
-            }
-            float o[PH];
-#pragma unroll
-            for (int c = 0; c < PH; ++c) o[c] = 0.f;
-#pragma unroll
-            for (int k = 0; k < Q; ++k)
-#pragma unroll
-                for (int c = 0; c < PH; c += 4) {
-                    const float4 w4 = *reinterpret_cast<const float4*>(swt + k * P + half * PH + c);
-                    o[c] = fmaf(yv[k], w4.x, o[c]);
-                    o[c + 1] = fmaf(yv[k], w4.y, o[c + 1]);
-                    o[c + 2] = fmaf(yv[k], w4.z, o[c + 2]);
-                    o[c + 3] = fmaf(yv[k], w4.w, o[c + 3]);
-                }
-            const float s = row_scale ? (float)srs[(size_t)buf * DB_ROWS + dr] : 1.f;
-            float4* out = reinterpret_cast<float4*>(dz + (r0 + dr) * P + half * PH);
-#pragma unroll
-            for (int c = 0; c < PH; c += 4) out[c / 4] = make_float4(s * o[c], s * o[c + 1], s * o[c + 2], s * o[c + 3]);
+        for (int s = 0; s < DB_STAGES - 1; ++s) load(s);
+        for (uint32_t blk = 0; blk < nblk; ++blk) {
+            load(blk + DB_STAGES - 1);  // refills the slot freed at the end of the previous iteration
+            asm volatile("cp.async.wait_group %0;" ::"n"(DB_STAGES - 1) : "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const uint32_t buf = blk % DB_STAGES;
+            const uint64_t r0 = r_begin + (uint64_t)blk * DB_ROWS;
+            const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)DB_ROWS ? r_end - r0 : (uint64_t)DB_ROWS);
+            work(buf, r0, nr, sdy + (size_t)buf * DB_ROWS * Q, sz + (size_t)buf * DB_ROWS * P);
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // slot `buf` is refilled next iteration
         }
-        // dW += z^T dy over this tile's rows (TI x TJ register tile per thread)
-        if (active) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    };
+    float* red = sm;  // [RG][P*Q] after the loop (the staging area is free)
+    constexpr uint32_t total = P * Q;
+    if (t < 128) {
+        // dz = row_scale * (dy W^T): 2 threads per row, PH outputs each
+        pipeline([&](uint32_t buf, uint64_t r0, uint32_t nr, const float* xdy, const float*) {
+            for (uint32_t it = t; it < 2 * DB_ROWS; it += 128) {
+                const uint32_t dr = it / 2, half = it % 2;
+                if (dr >= nr) break;
+                float yv[Q];
+#pragma unroll
+                for (int k = 0; k < Q; k += 2) {
+                    const float2 y2 = *reinterpret_cast<const float2*>(xdy + dr * Q + k);
+                    yv[k] = y2.x;
+                    yv[k + 1] = y2.y;
+                }
+                float o[PH];
+#pragma unroll
+                for (int c = 0; c < PH; ++c) o[c] = 0.f;
+#pragma unroll
+                for (int k = 0; k < Q; ++k)
+#pragma unroll
+                    for (int c = 0; c < PH; c += 4) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(swt + k * P + half * PH + c);
+                        o[c] = fmaf(yv[k], w4.x, o[c]);
+                        o[c + 1] = fmaf(yv[k], w4.y, o[c + 1]);
+                        o[c + 2] = fmaf(yv[k], w4.z, o[c + 2]);
+                        o[c + 3] = fmaf(yv[k], w4.w, o[c + 3]);
+                    }
+                const float s = row_scale ? (float)srs[(size_t)buf * DB_ROWS + dr] : 1.f;
+                float4* out = reinterpret_cast<float4*>(dz + (r0 + dr) * P + half * PH);
+#pragma unroll
+                for (int c = 0; c < PH; c += 4)
+                    out[c / 4] = make_float4(s * o[c], s * o[c + 1], s * o[c + 2], s * o[c + 3]);
+            }
+        });
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // the dW side writes its partials into `red`
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+    } else {
+        // dW += z^T dy (TI x TJ register tile per thread, RG row groups)
+        const uint32_t td = t - 128, grp = td / TILES, tile = td % TILES;
+        const bool active = grp < RG;
+        const uint32_t ti = (tile / TQ) * TI, tj = (tile % TQ) * TJ;
+        float acc[TI][TJ];
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+            for (int j = 0; j < TJ; ++j) acc[i][j] = 0.f;
+        pipeline([&](uint32_t, uint64_t, uint32_t nr, const float* xdy, const float* xz) {
+            if (!active) return;
             for (uint32_t k = grp; k < nr; k += RG) {
                 const float4 a4 = *reinterpret_cast<const float4*>(xz + k * P + ti);
                 float bv[TJ];
@@ -948,20 +969,16 @@ __global__ void __launch_bounds__(256) k6_dense_bwd(const float* __restrict__ dy
 #pragma unroll
                     for (int j = 0; j < TJ; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
             }
-        }
-        __syncthreads();  // slot `buf` is refilled by the next iteration's load
+        });
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // every role is out of the ring
+        if (active)
+#pragma unroll
+            for (int i = 0; i < TI; ++i)
+#pragma unroll
+                for (int j = 0; j < TJ; ++j)
+                    if (tj + j < Q) red[(size_t)grp * total + (ti + i) * Q + tj + j] = acc[i][j];
+        asm volatile("bar.sync 1, 256;" ::: "memory");
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    float* red = sm;  // [RG][P*Q] (staging area is free)
-    constexpr uint32_t total = P * Q;
-    if (active)
-#pragma unroll
-        for (int i = 0; i < TI; ++i)
-#pragma unroll
-            for (int j = 0; j < TJ; ++j)
-                if (tj + j < Q) red[(size_t)grp * total + (ti + i) * Q + tj + j] = acc[i][j];
-    __syncthreads();
     for (uint32_t o = t; o < total; o += blockDim.x) {
         float sum = 0.f;
         for (uint32_t g2 = 0; g2 < RG; ++g2) sum += red[(size_t)g2 * total + o];
@@ -972,7 +989,7 @@ __global__ void __launch_bounds__(256) k6_dense_bwd(const float* __restrict__ dy
 template <int P, int Q>
 void launch_dense_bwd(gnna_ctx* ctx, const float* dy, const float* w, const float* z, const double* rs, uint32_t m,
                       float* dz, float* dw) {
-    constexpr int TQ = (Q + 7) / 8, TILES = (P / 4) * TQ, RG = 256 / TILES;
+    constexpr int TQ = (Q + 7) / 8, TILES = (P / 4) * TQ, RG = 128 / TILES;
     const size_t sbytes = std::max<size_t>((size_t)(DB_STAGES * DB_ROWS * (P + Q) + Q * P + (Q * P) % 2 +
                                                     2 * DB_STAGES * DB_ROWS),
                                            (size_t)RG * P * Q) * 4;
