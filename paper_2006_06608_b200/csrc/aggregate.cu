@@ -716,6 +716,8 @@ Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const
     uint32_t t = dw_teams ? pow2ceil((dw + s.vec - 1) / s.vec) : 32u;
     t = std::min<uint32_t>(t, pow2ceil(nvec));
     t = std::min<uint32_t>(t, team_cap);
+    static const int team_max = std::getenv("GNNA_K3_TEAM_MAX") ? std::atoi(std::getenv("GNNA_K3_TEAM_MAX")) : 0;
+    if (team_max > 0) t = std::min<uint32_t>(t, (uint32_t)team_max);  // A/B: narrower teams, more units per warp
     t = std::max<uint32_t>(t, 1);
     s.team = std::min<uint32_t>(t, 32);
     s.kpl = (nvec + s.team - 1) / s.team;
