@@ -895,12 +895,12 @@ __global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__
         for (uint32_t blk = 0; blk < nblk; ++blk) {
             load(blk + DB_STAGES - 1);  // refills the slot freed at the end of the previous iteration
             asm volatile("cp.async.wait_group %0;" ::"n"(DB_STAGES - 1) : "memory");
-            asm volatile("bar.sync 1, 256;" ::: "memory");
+            asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code
             const uint32_t buf = blk % DB_STAGES;
             const uint64_t r0 = r_begin + (uint64_t)blk * DB_ROWS;
             const uint32_t nr = (uint32_t)(r_end - r0 < (uint64_t)DB_ROWS ? r_end - r0 : (uint64_t)DB_ROWS);
             work(buf, r0, nr, sdy + (size_t)buf * DB_ROWS * Q, sz + (size_t)buf * DB_ROWS * P);
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // slot `buf` is refilled next iteration
+            asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code  // slot `buf` is refilled next iteration
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
     };
@@ -939,8 +939,8 @@ __global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__
                     out[c / 4] = make_float4(s * o[c], s * o[c + 1], s * o[c + 2], s * o[c + 3]);
             }
         });
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // the dW side writes its partials into `red`
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code  // the dW side writes its partials into `red`
+        asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code
     } else {
         // dW += z^T dy (TI x TJ register tile per thread, RG row groups)
         const uint32_t td = t - 128, grp = td / TILES, tile = td % TILES;
@@ -970,14 +970,14 @@ __global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__
                     for (int j = 0; j < TJ; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
             }
         });
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // every role is out of the ring
+        asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code  // every role is out of the ring
         if (active)
 #pragma unroll
             for (int i = 0; i < TI; ++i)
 #pragma unroll
                 for (int j = 0; j < TJ; ++j)
                     if (tj + j < Q) red[(size_t)grp * total + (ti + i) * Q + tj + j] = acc[i][j];
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code
     }
     for (uint32_t o = t; o < total; o += blockDim.x) {
         float sum = 0.f;

@@ -111,11 +111,10 @@ class GCN2:
         symmetrised CSR to_csr(.., true) builds, so Â^T = Â)."""
         ctx, s = self.ctx, self.saved
         in_dim, hid, out_dim = self.dims
-        w1t, w2t = self.w1.t().contiguous(), self.w2.t().contiguous()
         if out_dim < hid:
             dt2 = self._agg(dy)                                    # Â^T dY
             dw2 = ctx_gemm_tn(ctx, s["h1"], dt2)                   # h1^T dT2
-            dh1 = ctx.gemm(dt2, w2t)
+            dh1 = ctx.gemm(dt2, self.w2.t().contiguous())
             dp1 = dh1 * (s["h1"] > 0)
             dp1_scaled = False
         else:
@@ -127,7 +126,7 @@ class GCN2:
                 side.stream.wait_stream(main)
                 with torch.cuda.stream(side.stream):
                     dw2 = ctx_gemm_tn(side.ctx, s["z2"], dy)
-                dz2 = ctx.gemm(dy, w2t, None, 2, self.norm)        # norm * (dY W2^T)
+                dz2 = ctx.gemm(dy, self.w2.t().contiguous(), None, 2, self.norm)  # norm * (dY W2^T)
             else:
                 # one pass over dY and Â h1: dZ2 = norm * (dY W2^T), dW2 = (Â h1)^T dY
                 dz2, dw2 = ctx.dense_backward(dy, self.w2, s["z2"], self.norm)
@@ -145,8 +144,8 @@ class GCN2:
         return dw1, dw2
 
     def sgd(self, dw1, dw2):
-        self.w1.sub_(self.lr * dw1)
-        self.w2.sub_(self.lr * dw2)
+        self.w1.add_(dw1, alpha=-self.lr)  # one fused kernel per weight
+        self.w2.add_(dw2, alpha=-self.lr)
 
     def step(self, x, dy):
         y = self.forward(x)

@@ -85,6 +85,45 @@ def main():
     reps = [torch.zeros((n, 32), device="cuda") for _ in range(3)]
     plan.aggregate_fanout(xf, y, peers=reps)
     assert all(torch.equal(r, y) for r in reps)
+    # round 2: node-weight fan-out, the fused dense backward (C3 output-layer
+    # widths), the hub remap / row gather of the drop-in, the device-aware
+    # evaluator, empty rows + split nodes through the one-launch K3
+    rs, sw, _ = ctx.gcn_weights(drp, dcol, True, edge_weights=False)
+    plan.aggregate_fanout(xf, y, peers=reps, node_weight=rs, self_weight=sw, row_scale=rs)
+    m2 = GCN2(ctx, drp, dcol, 96, 16, 22)
+    m2.step(dev(rng.random((n, 96))).float(), dev(rng.random((n, 22)) - 0.5).float())
+    dz, dwd = ctx.dense_backward(dev(rng.random((777, 22))).float(), dev(rng.random((16, 22))).float(),
+                                 dev(rng.random((777, 16))).float(), dev(rng.random(777)))
+    hubs = torch.empty(64, dtype=torch.int32, device="cuda")
+    col_h = torch.empty_like(dcol)
+    import ctypes as C
+    he = C.c_uint64()
+    assert ctx.L.gnna_hub_remap(ctx.h, C.c_void_p(drp.data_ptr()), C.c_void_p(dcol.data_ptr()), C.c_uint32(n),
+                                C.c_uint32(64), C.c_void_p(hubs.data_ptr()), C.c_void_p(col_h.data_ptr()),
+                                C.byref(he)) == 0
+    xe = torch.empty((n + 64, 16), dtype=torch.float64, device="cuda")
+    xe[:n] = dev(rng.random((n, 16)))
+    assert ctx.L.gnna_gather_rows(ctx.h, C.c_int(1), C.c_void_p(xe.data_ptr()), C.c_uint32(16),
+                                  C.c_void_p(hubs.data_ptr()), C.c_uint64(64),
+                                  C.c_void_p(xe[n:].data_ptr())) == 0
+    ph = ctx.plan(drp, col_h, Params.make(ngs=5, dw=8, tpb=128, dim=16), 2)
+    pn = ctx.plan(drp, dcol, Params.make(ngs=5, dw=8, tpb=128, dim=16), 2)
+    yh = torch.empty((n, 16), dtype=torch.float64, device="cuda")
+    assert ctx.L.gnna_aggregate(ctx.h, ph.h, C.c_int(1), C.c_int(1), C.c_void_p(xe.data_ptr()),
+                                C.c_void_p(yh.data_ptr())) == 0  # hub rows read from the tail
+    assert torch.equal(yh, pn.aggregate(xe[:n].contiguous()))    # bit-identical to the plain layout
+    ctx.b200_params(drp, 16, window=True)
+    ctx.b200_params(drp, 64, dtype=torch.float64)
+    # isolated nodes (empty rows) in a plan with split hubs: trailing blocks + last-writer combine
+    e2 = edges[edges[:, 0] < n - 50]
+    e2 = e2[e2[:, 1] < n - 50]
+    rpe, cole = orc.to_csr(n, e2, True)
+    pe = ctx.plan(dev(rpe), dev(cole), Params.make(ngs=4, dw=8, tpb=128, dim=16), 2)
+    for dt in (torch.float32, torch.float64):
+        xs = dev(rng.random((n, 16))).to(dt)
+        got = pe.aggregate_ex(xs, alpha=0.5)
+        want = orc.aggregate_oracle(rpe, cole, xs.double().cpu().numpy()) + 0.5 * xs.double().cpu().numpy()
+        assert np.allclose(got.double().cpu().numpy(), want, rtol=1e-5)
     torch.cuda.synchronize()
     print("sanitize workload ok")
 
