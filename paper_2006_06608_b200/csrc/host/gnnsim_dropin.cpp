@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <sys/mman.h>
 #include <fstream>
 #include <atomic>
@@ -611,7 +612,14 @@ std::pair<FeatureMatrix, CostReport> aggregate_scheduled(const CsrGraph& g, cons
     // the output's host allocation (zero-filled, first-touch page faults: the
     // largest host cost at C3 / C4) proceeds on a helper thread meanwhile
     std::unique_ptr<FeatureMatrix> yp;
-    std::thread alloc([&] { yp = std::make_unique<FeatureMatrix>(host_features(g.num_nodes, x.dim)); });
+    std::exception_ptr alloc_err;
+    std::thread alloc([&] {
+        try {
+            yp = std::make_unique<FeatureMatrix>(host_features(g.num_nodes, x.dim));
+        } catch (...) {
+            alloc_err = std::current_exception();  // rethrown on the caller's thread after the join
+        }
+    });
     struct Join {
         std::thread& t;
         ~Join() {
@@ -647,6 +655,7 @@ std::pair<FeatureMatrix, CostReport> aggregate_scheduled(const CsrGraph& g, cons
     ok(gnna_synchronize(ctx()));
     pt.mark("aggregate+cost");
     alloc.join();
+    if (alloc_err) std::rethrow_exception(alloc_err);
     FeatureMatrix y = std::move(*yp);
     pt.mark("alloc_y (join)");
     dy.to(y.values.data(), y.values.size());
