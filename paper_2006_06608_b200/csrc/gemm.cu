@@ -919,24 +919,25 @@ __global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__
                     yv[k] = y2.x;
                     yv[k + 1] = y2.y;
                 }
-                float o[PH];
+                // packed FFMA2 (two lanes of one fma.rn each: the same roundings as scalar fmaf)
+                float2 o[PH / 2];
 #pragma unroll
-                for (int c = 0; c < PH; ++c) o[c] = 0.f;
+                for (int c = 0; c < PH / 2; ++c) o[c] = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int k = 0; k < Q; ++k)
+                for (int k = 0; k < Q; ++k) {
+                    const float2 yk = make_float2(yv[k], yv[k]);
 #pragma unroll
                     for (int c = 0; c < PH; c += 4) {
                         const float4 w4 = *reinterpret_cast<const float4*>(swt + k * P + half * PH + c);
-                        o[c] = fmaf(yv[k], w4.x, o[c]);
-                        o[c + 1] = fmaf(yv[k], w4.y, o[c + 1]);
-                        o[c + 2] = fmaf(yv[k], w4.z, o[c + 2]);
-                        o[c + 3] = fmaf(yv[k], w4.w, o[c + 3]);
+                        o[c / 2] = __ffma2_rn(yk, make_float2(w4.x, w4.y), o[c / 2]);
+                        o[c / 2 + 1] = __ffma2_rn(yk, make_float2(w4.z, w4.w), o[c / 2 + 1]);
                     }
+                }
                 const float s = row_scale ? (float)srs[(size_t)buf * DB_ROWS + dr] : 1.f;
                 float4* out = reinterpret_cast<float4*>(dz + (r0 + dr) * P + half * PH);
 #pragma unroll
                 for (int c = 0; c < PH; c += 4)
-                    out[c / 4] = make_float4(s * o[c], s * o[c + 1], s * o[c + 2], s * o[c + 3]);
+                    out[c / 4] = make_float4(s * o[c / 2].x, s * o[c / 2].y, s * o[c / 2 + 1].x, s * o[c / 2 + 1].y);
             }
         });
         asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code  // the dW side writes its partials into `red`
@@ -946,28 +947,26 @@ __global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__
         const uint32_t td = t - 128, grp = td / TILES, tile = td % TILES;
         const bool active = grp < RG;
         const uint32_t ti = (tile / TQ) * TI, tj = (tile % TQ) * TJ;
-        float acc[TI][TJ];
+        float2 acc[TI][TJ / 2];  // column pairs: packed FFMA2
 #pragma unroll
         for (int i = 0; i < TI; ++i)
 #pragma unroll
-            for (int j = 0; j < TJ; ++j) acc[i][j] = 0.f;
+            for (int j = 0; j < TJ / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
         pipeline([&](uint32_t, uint64_t, uint32_t nr, const float* xdy, const float* xz) {
             if (!active) return;
             for (uint32_t k = grp; k < nr; k += RG) {
                 const float4 a4 = *reinterpret_cast<const float4*>(xz + k * P + ti);
-                float bv[TJ];
+                float2 bv[TJ / 2];
 #pragma unroll
-                for (int j = 0; j < TJ; j += 2) {
-                    const float2 b2 = tj + j < Q ? *reinterpret_cast<const float2*>(xdy + k * Q + tj + j)
-                                                 : make_float2(0.f, 0.f);
-                    bv[j] = b2.x;
-                    bv[j + 1] = b2.y;
-                }
+                for (int j = 0; j < TJ; j += 2)
+                    bv[j / 2] = tj + j < Q ? *reinterpret_cast<const float2*>(xdy + k * Q + tj + j)
+                                           : make_float2(0.f, 0.f);
                 const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
                 for (int i = 0; i < TI; ++i)
 #pragma unroll
-                    for (int j = 0; j < TJ; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                    for (int j = 0; j < TJ / 2; ++j)
+                        acc[i][j] = __ffma2_rn(make_float2(av[i], av[i]), bv[j], acc[i][j]);
             }
         });
         asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code  // every role is out of the ring
@@ -976,7 +975,8 @@ __global__ void __launch_bounds__(256, 4) k6_dense_bwd(const float* __restrict__
             for (int i = 0; i < TI; ++i)
 #pragma unroll
                 for (int j = 0; j < TJ; ++j)
-                    if (tj + j < Q) red[(size_t)grp * total + (ti + i) * Q + tj + j] = acc[i][j];
+                    if (tj + j < Q)
+                        red[(size_t)grp * total + (ti + i) * Q + tj + j] = j % 2 ? acc[i][j / 2].y : acc[i][j / 2].x;
         asm volatile("barrier.sync 1, 256;" ::: "memory");  // non-.aligned: the roles reach it from different code
     }
     for (uint32_t o = t; o < total; o += blockDim.x) {

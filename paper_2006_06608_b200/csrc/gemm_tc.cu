@@ -20,7 +20,7 @@
 //     against [W_hi ; W_lo] (N = 2*NP: both cross terms in one instruction);
 //   * two groups of 4 warps take alternate tiles: each thread (= TMEM lane =
 //     tile row) reads its row from the swizzled stage (conflict-free), writes
-//     A_lo = rna_tf32(x - trunc(x)) into TMEM with tcgen05.st, and the MMA
+//     A_lo = x - trunc(x) (lo_part2) into TMEM with tcgen05.st, and the MMA
 //     warp runs A_lo x W_hi with A from TMEM; the group then tcgen05.ld's its
 //     accumulator, adds the hi/lo column halves, applies the fused epilogue
 //     and stores the 32-row run of each warp coalesced via shared memory.
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(TM) k6_gemm_tc(TcArgs g) {
 // cp.async.bulk.tensor (box 32 fp32 x 128 rows per K slice, SWIZZLE_128B),
 // which IS the canonical SW128 K-major operand layout, so the raw fp32 tile
 // is A_hi as the tensor core reads it (tf32 = the top 19 bits).  The only
-// register pass is lo = rna_tf32(x - trunc_tf32(x)) written elementwise at the
+// register pass is lo = x - trunc_tf32(x) (lo_part2) written elementwise at the
 // same offsets (linear, conflict-free).  An S-deep ring of stages keeps S
 // tiles of HBM reads in flight while the CTA converts, multiplies and writes.
 // Two MMAs per K step: A_hi x [W_hi ; W_lo] (N = 2*NP, TMEM columns
@@ -318,6 +318,23 @@ struct TmaCfg {
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __device__ __forceinline__ float lo_part(float x) { return rna_tf32(x - trunc_tf32(x)); }
+
+// The converters' split of a streamed operand: the MMA reads an fp32 operand
+// as tf32 by dropping its low 13 bits, so the raw x serves as hi, and
+// lo = x - trunc(x) (exact in fp32) as the correction, which the MMA
+// truncates in turn: error <= 2^-20 |x| per operand, against 2^-21 when lo is
+// rounded to nearest first (GNNA_TF32_LO_RNA=1, three more instructions per
+// element).  Two elements per packed FADD2.
+#ifndef GNNA_TF32_LO_RNA
+#define GNNA_TF32_LO_RNA 0
+#endif
+__device__ __forceinline__ float2 lo_part2(float a, float b) {
+#if GNNA_TF32_LO_RNA
+    return make_float2(lo_part(a), lo_part(b));
+#else
+    return __fadd2_rn(make_float2(a, b), make_float2(-trunc_tf32(a), -trunc_tf32(b)));
+#endif
+}
 
 // 16 registers -> 16 consecutive TMEM columns of this warp's 32 lanes.
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
@@ -471,7 +488,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
             {
                 const uint32_t s = i % S, b = i & 1u;
                 mbar_wait(smem_u32(&full[s]), (i / S) & 1u);
-                // lo = rna_tf32(x - trunc_tf32(x)) of this thread's row, read from the
+                // lo = x - trunc_tf32(x) of this thread's row (lo_part2), read from the
                 // swizzled tile (8 consecutive lanes hit 8 distinct bank groups)
                 const unsigned char* stg = base_p + s * C::STAGE + row_off;
 #pragma unroll
@@ -483,8 +500,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
                     float lo[32];
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
-                        lo[4 * c] = lo_part(x[c].x), lo[4 * c + 1] = lo_part(x[c].y);
-                        lo[4 * c + 2] = lo_part(x[c].z), lo[4 * c + 3] = lo_part(x[c].w);
+                        const float2 l01 = lo_part2(x[c].x, x[c].y), l23 = lo_part2(x[c].z, x[c].w);
+                        lo[4 * c] = l01.x, lo[4 * c + 1] = l01.y, lo[4 * c + 2] = l23.x, lo[4 * c + 3] = l23.y;
                     }
                     const uint32_t col = tmem + lane_off + C::LO0 + b * KP + sl * 32;
                     tmem_st16(col, lo);
@@ -651,7 +668,7 @@ void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
 // 512-byte K atoms; the TMA mode CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes
 // exactly that, so the raw TMA'd stage IS A_hi / B_hi.
 //   * stage (S-deep ring): A[PS slices] | B_hi[QS] | B_lo[QS], where B_lo =
-//     rna_tf32(x - trunc(x)) is written elementwise by the converter warps at
+//     x - trunc(x) (lo_part2) is written elementwise by the converter warps at
 //     the same swizzled offsets, one LBO after B_hi: [B_hi | B_lo] is ONE
 //     N = 64*QS operand;
 //   * A_lo goes to TMEM (K-major there: lane = feature, column = row),
@@ -665,7 +682,16 @@ void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
 // Per-CTA partials are summed by k_reduce_partials in a fixed slice order
 // (deterministic; GNNA_TN_SEQ_REDUCE=1 keeps the sequential CTA-order k6_tn_reduce).
 // ---------------------------------------------------------------------------
-constexpr int TN_BK = 64;
+#ifndef GNNA_TN_BK
+#define GNNA_TN_BK 64
+#endif
+#ifndef GNNA_TN_SMAX
+#define GNNA_TN_SMAX 8
+#endif
+#ifndef GNNA_TN_LOB
+#define GNNA_TN_LOB 4
+#endif
+constexpr int TN_BK = GNNA_TN_BK;  // rows per block (one TMA box per 32-feature slice)
 
 template <int PS, int QS>
 struct TnCfg {
@@ -674,10 +700,10 @@ struct TnCfg {
     static constexpr uint32_t STAGE = (PS + 2 * QS) * SL;
     static constexpr uint32_t TAIL = (4 - PS) * SL;  // phantom A slices past the last stage
     static constexpr int S0 = (int)((224u * 1024u - TAIL) / STAGE);
-    static constexpr int S = S0 > 8 ? 8 : S0;
+    static constexpr int S = S0 > GNNA_TN_SMAX ? GNNA_TN_SMAX : S0;
     static constexpr size_t SMEM = (size_t)S * STAGE + TAIL + 1024;
     static constexpr uint32_t ND = 64 * QS;                  // accumulator columns [hi.hi | hi.lo]
-    static constexpr int LOB = 4;                           // A_lo ring depth (TMEM)
+    static constexpr int LOB = GNNA_TN_LOB;                 // A_lo ring depth (TMEM)
     static constexpr uint32_t LO0 = ND < 32 ? 32 : ND;      // A_lo buffers: LOB x BK columns
     static constexpr uint32_t NEED = LO0 + LOB * TN_BK;
     static constexpr uint32_t TCOLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
@@ -707,8 +733,11 @@ struct TnArgs {
 
 constexpr int TN_THREADS = TM + 32;
 
-template <int PS, int QS>
-__global__ void __launch_bounds__(TN_THREADS, 1) k6_gemm_tn_tc(const __grid_constant__ CUtensorMap amap,
+// PROD: a sixth warp refills the ring (waits each stage's `empty` in order
+// and re-issues its TMA) instead of the MMA warp between MMAs, so a refill
+// never waits for the converters of the next block.
+template <int PS, int QS, bool PROD>
+__global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid_constant__ CUtensorMap amap,
                                                                const __grid_constant__ CUtensorMap bmap, TnArgs g) {
     using C = TnCfg<PS, QS>;
     constexpr int S = C::S;
@@ -797,13 +826,19 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k6_gemm_tn_tc(const __grid_cons
                     : "memory");
             }
             __syncwarp();
-            if (i >= 1) {
+            if (!PROD && i >= 1) {
                 const uint32_t j = i - 1;
                 mbar_wait(smem_u32(&empty[j % S]), (j / S) & 1u);
                 if (lane == 0 && j + S < nb) issue(j + S);
                 __syncwarp();
             }
         }
+    } else if (warp == 5) {
+        if (PROD && lane == 0)
+            for (uint32_t i = S; i < nb; ++i) {
+                mbar_wait(smem_u32(&empty[(i - S) % S]), ((i - S) / S) & 1u);
+                issue(i);
+            }
     } else {
         const uint32_t lane_off = (warp * 32u) << 16;
         for (uint32_t i = 0; i < nb; ++i) {
@@ -820,11 +855,16 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k6_gemm_tn_tc(const __grid_cons
                 for (int k0 = 0; k0 < TN_BK; k0 += 16) {
                     float lo[16];
 #pragma unroll
-                    for (int kk = 0; kk < 16; ++kk) {
-                        const uint32_t k = k0 + kk;
-                        const float x = *reinterpret_cast<const float*>(sa + (k / 4) * 512 + (k % 4) * 128 +
-                                                                        ((c32 ^ (k % 4)) * 32) + w4);
-                        lo[kk] = lo_part(x);
+                    for (int kk = 0; kk < 16; kk += 2) {
+                        float x[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const uint32_t k = k0 + kk + h;
+                            x[h] = *reinterpret_cast<const float*>(sa + (k / 4) * 512 + (k % 4) * 128 +
+                                                                   ((c32 ^ (k % 4)) * 32) + w4);
+                        }
+                        const float2 l = lo_part2(x[0], x[1]);
+                        lo[kk] = l.x, lo[kk + 1] = l.y;
                     }
                     tmem_st16(tmem + lane_off + C::LO0 + b * TN_BK + k0, lo);
                 }
@@ -834,7 +874,7 @@ __global__ void __launch_bounds__(TN_THREADS, 1) k6_gemm_tn_tc(const __grid_cons
             for (uint32_t f = t; f < QS * (C::SL / 16); f += TM) {
                 const float4 x = reinterpret_cast<const float4*>(st + C::BH)[f];
                 reinterpret_cast<float4*>(const_cast<unsigned char*>(st) + C::BL)[f] =
-                    make_float4(lo_part(x.x), lo_part(x.y), lo_part(x.z), lo_part(x.w));
+                    make_float4(lo_part2(x.x, x.y).x, lo_part2(x.x, x.y).y, lo_part2(x.z, x.w).x, lo_part2(x.z, x.w).y);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -896,7 +936,11 @@ bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uin
         !make_map(&bmap, b, q, m, TN_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
         return false;
     using C = TnCfg<PS, QS>;
-    auto kern = k6_gemm_tn_tc<PS, QS>;
+    static const bool prod = [] {
+        const char* e = std::getenv("GNNA_TN_PROD");  // A/B switch (0: the MMA warp refills)
+        return !(e && *e == '0');
+    }();
+    auto kern = prod ? k6_gemm_tn_tc<PS, QS, true> : k6_gemm_tn_tc<PS, QS, false>;
     static std::atomic<uint64_t> attr{0};
     smem_attr_once(attr, kern, ctx->device, C::SMEM);
     const uint32_t nblk = (m + TN_BK - 1) / TN_BK;
@@ -906,7 +950,7 @@ bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uin
     const uint32_t total = p * q;
     DevBuf<float> part((size_t)ctas * total, ctx->stream);
     TnArgs g{m, p, q, nblk, bpc, part.get()};
-    kern<<<ctas, TN_THREADS, C::SMEM, ctx->stream>>>(amap, bmap, g);
+    kern<<<ctas, TN_THREADS + (prod ? 32 : 0), C::SMEM, ctx->stream>>>(amap, bmap, g);
     launched(ctx, "k6_gemm_tn_tc");
     static const bool seq = std::getenv("GNNA_TN_SEQ_REDUCE") != nullptr;  // A/B switch
     if (seq) {

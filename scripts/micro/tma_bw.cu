@@ -1,0 +1,131 @@
+// Microbenchmark: streaming read bandwidth of TMA 2D/3D tile loads into an
+// S-deep shared-memory ring (one CTA per SM, one producer thread, one
+// consumer warp that releases each stage as soon as it lands).  Box =
+// {32 floats, R rows} x 3 column slices of a 96-wide row-major fp32 matrix
+// (the shape k6_gemm_tn_tc / k6_gemm_tc_tma read), either as 3 TMA ops per
+// block (2D map) or one (3D map: {32 cols, rows, 3 slices}).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tma_bw tma_bw.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+#include <vector>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void wait(uint32_t bar, uint32_t ph) {
+    asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(bar), "r"(ph) : "memory");
+}
+
+template <int R, int S, bool D3>
+__global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap map, uint32_t nblk, uint32_t bpc, unsigned long long* sink) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ uint64_t full[S], empty[S];
+    const uint32_t base = (su32(sm) + 1023u) & ~1023u;
+    constexpr uint32_t SLB = R * 128, ST = 3 * SLB;
+    const uint32_t b0 = blockIdx.x * bpc;
+    const uint32_t nb = b0 >= nblk ? 0 : (nblk - b0 < bpc ? nblk - b0 : bpc);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t i) {
+        const uint32_t s = i % S, row = (b0 + i) * R, bar = su32(&full[s]), st = base + s * ST;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(ST) : "memory");
+        if (D3) {
+            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                         ::"r"(st), "l"((uint64_t)&map), "r"(0), "r"(row), "r"(0), "r"(bar) : "memory");
+        } else {
+            for (int sl = 0; sl < 3; ++sl)
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                             ::"r"(st + sl * SLB), "l"((uint64_t)&map), "r"(sl * 32), "r"(row), "r"(bar) : "memory");
+        }
+    };
+    unsigned long long acc = 0;
+    if (threadIdx.x == 0) {
+        for (uint32_t i = 0; i < nb; ++i) {
+            if (i >= S) wait(su32(&empty[i % S]), ((i - S) / S) & 1u);
+            issue(i);
+        }
+    } else if (threadIdx.x == 32) {
+        for (uint32_t i = 0; i < nb; ++i) {
+            wait(su32(&full[i % S]), (i / S) & 1u);
+            acc += *reinterpret_cast<const uint32_t*>(sm + (base - su32(sm)) + (i % S) * ST);
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[i % S])) : "memory");
+        }
+        sink[blockIdx.x] = acc;
+    }
+}
+
+typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <int R, int S, bool D3>
+void run(Enc enc, float* x, uint64_t m, int sms, unsigned long long* sink) {
+    CUtensorMap map;
+    CUresult rc;
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (D3) {
+        const cuuint64_t dims[3] = {32, m, 3};
+        const cuuint64_t strides[2] = {96 * 4, 128};
+        const cuuint32_t box[3] = {32, R, 3};
+        rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        const cuuint64_t dims[2] = {96, m};
+        const cuuint64_t strides[1] = {96 * 4};
+        const cuuint32_t box[2] = {32, R};
+        rc = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, x, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (rc != CUDA_SUCCESS) { printf("{\"R\": %d, \"S\": %d, \"d3\": %d, \"encode_error\": %d}\n", R, S, (int)D3, (int)rc); return; }
+    const size_t smem = (size_t)S * 3 * R * 128 + 1024;
+    if (smem > 227 * 1024) return;
+    cudaFuncSetAttribute(k<R, S, D3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint32_t nblk = (uint32_t)(m / R), bpc = (nblk + sms - 1) / sms, ctas = (nblk + bpc - 1) / bpc;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        cudaEventRecord(a);
+        k<R, S, D3><<<ctas, 64, smem>>>(map, nblk, bpc, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        if (rep) best = ms < best ? ms : best;
+    }
+    cudaError_t e = cudaGetLastError();
+    const double bytes = (double)nblk * R * 96 * 4;
+    printf("{\"R\": %d, \"S\": %d, \"d3\": %d, \"inflight_kb\": %d, \"ms\": %.4f, \"GBps\": %.1f, \"err\": \"%s\"}\n", R, S, (int)D3,
+           S * 3 * R * 128 / 1024, best, bytes / best / 1e6, cudaGetErrorString(e));
+}
+
+int main() {
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    void* p = nullptr; cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    Enc enc = (Enc)p;
+    const uint64_t m = 4u << 20;  // 4M rows x 96 f32 = 1.6 GB (>> L2)
+    float* x; cudaMalloc(&x, m * 96 * 4); cudaMemset(x, 0, m * 96 * 4);
+    unsigned long long* sink; cudaMalloc(&sink, 4096 * 8);
+    run<64, 2, false>(enc, x, m, sms, sink);
+    run<64, 3, false>(enc, x, m, sms, sink);
+    run<64, 5, false>(enc, x, m, sms, sink);
+    run<64, 8, false>(enc, x, m, sms, sink);
+    run<64, 5, true>(enc, x, m, sms, sink);
+    run<64, 8, true>(enc, x, m, sms, sink);
+    run<128, 2, false>(enc, x, m, sms, sink);
+    run<128, 3, false>(enc, x, m, sms, sink);
+    run<128, 4, false>(enc, x, m, sms, sink);
+    run<128, 4, true>(enc, x, m, sms, sink);
+    run<32, 8, false>(enc, x, m, sms, sink);
+    run<32, 16, false>(enc, x, m, sms, sink);
+    run<32, 16, true>(enc, x, m, sms, sink);
+    run<256, 2, false>(enc, x, m, sms, sink);
+    run<256, 2, true>(enc, x, m, sms, sink);
+    return 0;
+}
