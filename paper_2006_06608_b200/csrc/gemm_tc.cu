@@ -682,30 +682,29 @@ void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
 // Per-CTA partials are summed by k_reduce_partials in a fixed slice order
 // (deterministic; GNNA_TN_SEQ_REDUCE=1 keeps the sequential CTA-order k6_tn_reduce).
 // ---------------------------------------------------------------------------
-#ifndef GNNA_TN_BK
-#define GNNA_TN_BK 64
-#endif
-#ifndef GNNA_TN_SMAX
-#define GNNA_TN_SMAX 8
-#endif
-#ifndef GNNA_TN_LOB
-#define GNNA_TN_LOB 4
-#endif
-constexpr int TN_BK = GNNA_TN_BK;  // rows per block (one TMA box per 32-feature slice)
-
-template <int PS, int QS>
+// QS = 0 is the packed form for q <= 16: ONE B slice holds [B_hi | B_lo]
+// (the TMA writes B into columns 0-15, the columns past q arrive zero-filled,
+// and the converters write B_lo into columns 16-31 of the same swizzled
+// rows), so the SS MMA is N = 32 and the stage has no separate B_lo slice.
+// BK = rows per block (one TMA box per 32-feature slice): 128 where three
+// such stages fit, else 64.  Each tcgen05.mma here is M 128 x N 32..64 x K 8,
+// which costs a fixed ~45 cycles (scripts/micro/mma_rate.cu), so a block's
+// MMA time is its instruction count; bigger blocks halve the per-block
+// handoffs and commits (C3 dW1: 43.4 -> 39.0 us).
+template <int PS, int QS, int BK>
 struct TnCfg {
-    static constexpr uint32_t SL = TN_BK * 128;  // one 32-feature slice of a block (8 KB)
-    static constexpr uint32_t AH = 0, BH = PS * SL, BL = BH + QS * SL;
-    static constexpr uint32_t STAGE = (PS + 2 * QS) * SL;
+    static constexpr uint32_t SL = BK * 128;  // one 32-feature slice of a block (8 / 16 KB)
+    static constexpr uint32_t QB = QS ? QS : 1;  // B slices the TMA loads
+    static constexpr uint32_t AH = 0, BH = PS * SL, BL = BH + QB * SL;
+    static constexpr uint32_t STAGE = (PS + QB + QS) * SL;
     static constexpr uint32_t TAIL = (4 - PS) * SL;  // phantom A slices past the last stage
     static constexpr int S0 = (int)((224u * 1024u - TAIL) / STAGE);
-    static constexpr int S = S0 > GNNA_TN_SMAX ? GNNA_TN_SMAX : S0;
+    static constexpr int S = S0 > 8 ? 8 : S0;
     static constexpr size_t SMEM = (size_t)S * STAGE + TAIL + 1024;
-    static constexpr uint32_t ND = 64 * QS;                  // accumulator columns [hi.hi | hi.lo]
-    static constexpr int LOB = GNNA_TN_LOB;                 // A_lo ring depth (TMEM)
-    static constexpr uint32_t LO0 = ND < 32 ? 32 : ND;      // A_lo buffers: LOB x BK columns
-    static constexpr uint32_t NEED = LO0 + LOB * TN_BK;
+    static constexpr uint32_t ND = QS ? 64 * QS : 32;        // accumulator columns [hi.hi | hi.lo]
+    static constexpr int LOB = BK >= 128 ? 3 : 4;           // A_lo ring depth (TMEM)
+    static constexpr uint32_t LO0 = ND;                     // A_lo buffers: LOB x BK columns
+    static constexpr uint32_t NEED = LO0 + LOB * BK;
     static constexpr uint32_t TCOLS = NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
     static_assert(NEED <= 512, "TMEM");
 };
@@ -736,10 +735,10 @@ constexpr int TN_THREADS = TM + 32;
 // PROD: a sixth warp refills the ring (waits each stage's `empty` in order
 // and re-issues its TMA) instead of the MMA warp between MMAs, so a refill
 // never waits for the converters of the next block.
-template <int PS, int QS, bool PROD>
+template <int PS, int QS, int BK, bool PROD>
 __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid_constant__ CUtensorMap amap,
                                                                const __grid_constant__ CUtensorMap bmap, TnArgs g) {
-    using C = TnCfg<PS, QS>;
+    using C = TnCfg<PS, QS, BK>;
     constexpr int S = C::S;
     static_assert(S >= 2, "stages");
     extern __shared__ unsigned char smem_raw[];
@@ -752,10 +751,10 @@ __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid
     const uint32_t t = threadIdx.x, warp = t / 32, lane = t % 32;
     const uint32_t b0 = blockIdx.x * g.bpc;
     const uint32_t nb = b0 >= g.nblk ? 0u : (g.nblk - b0 < g.bpc ? g.nblk - b0 : g.bpc);
-    constexpr uint32_t tx = (PS + QS) * C::SL;
+    constexpr uint32_t tx = (PS + C::QB) * C::SL;
 
     auto issue = [&](uint32_t i) {  // one thread: TMA of local block i into stage i % S
-        const uint32_t s = i % S, row = (b0 + i) * TN_BK;
+        const uint32_t s = i % S, row = (b0 + i) * BK;
         const uint32_t bar = smem_u32(&full[s]), st = base + s * C::STAGE;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
 #pragma unroll
@@ -766,7 +765,7 @@ __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid
                 "l"(reinterpret_cast<uint64_t>(&amap)), "r"(sl * 32), "r"(row), "r"(bar)
                 : "memory");
 #pragma unroll
-        for (int sl = 0; sl < QS; ++sl)
+        for (int sl = 0; sl < (int)C::QB; ++sl)
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
                 "[%4];" ::"r"(st + C::BH + sl * C::SL),
@@ -799,17 +798,18 @@ __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid
     const uint32_t tmem = tmem_slot;
 
     if (warp == 4) {
-        constexpr uint32_t ID_SS = idesc_tf32_mj<64 * QS, 1, 1>();
-        constexpr uint32_t ID_TS = idesc_tf32_mj<32 * QS, 0, 1>();
+        // packed: A_lo x [B_hi | B_lo] adds the lo x lo term to columns 16-31 as well
+        constexpr uint32_t ID_SS = idesc_tf32_mj<C::ND, 1, 1>();
+        constexpr uint32_t ID_TS = idesc_tf32_mj<QS ? 32 * QS : 32, 0, 1>();
         for (uint32_t i = 0; i < nb; ++i) {
             const uint32_t s = i % S, b = i % LOB;
             mbar_wait(smem_u32(&ready[b]), (i / LOB) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
                 const uint32_t st = base + s * C::STAGE;
-                const uint32_t alo = tmem + C::LO0 + b * TN_BK;
+                const uint32_t alo = tmem + C::LO0 + b * BK;
 #pragma unroll
-                for (int k8 = 0; k8 < TN_BK / 8; ++k8) {
+                for (int k8 = 0; k8 < BK / 8; ++k8) {
                     const uint32_t ko = k8 * 1024;
                     const uint64_t da = smem_desc_mn128(st + C::AH + ko, C::SL);
                     const uint64_t dbh = smem_desc_mn128(st + C::BH + ko, C::SL);
@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid
                 const unsigned char* sa = st + C::AH + warp * C::SL;
                 const uint32_t c32 = lane / 8, w4 = (lane % 8) * 4;
 #pragma unroll
-                for (int k0 = 0; k0 < TN_BK; k0 += 16) {
+                for (int k0 = 0; k0 < BK; k0 += 16) {
                     float lo[16];
 #pragma unroll
                     for (int kk = 0; kk < 16; kk += 2) {
@@ -866,15 +866,32 @@ __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid
                         const float2 l = lo_part2(x[0], x[1]);
                         lo[kk] = l.x, lo[kk + 1] = l.y;
                     }
-                    tmem_st16(tmem + lane_off + C::LO0 + b * TN_BK + k0, lo);
+                    tmem_st16(tmem + lane_off + C::LO0 + b * BK + k0, lo);
                 }
             }
-            // B_lo, elementwise at the same swizzled offsets
+            if constexpr (QS == 0) {
+                // B_lo of row k, 32-byte chunk j (columns 8j..8j+7) -> chunk j + 2 of the same row
+                for (uint32_t f = t; f < 2u * BK; f += TM) {
+                    const uint32_t k = f / 2, j = f % 2, row = (k / 4) * 512 + (k % 4) * 128;
+                    const float4* src = reinterpret_cast<const float4*>(st + C::BH + row + ((j ^ (k % 4)) * 32));
+                    float4* dst = reinterpret_cast<float4*>(const_cast<unsigned char*>(st) + C::BH + row +
+                                                            (((j + 2) ^ (k % 4)) * 32));
 #pragma unroll
-            for (uint32_t f = t; f < QS * (C::SL / 16); f += TM) {
-                const float4 x = reinterpret_cast<const float4*>(st + C::BH)[f];
-                reinterpret_cast<float4*>(const_cast<unsigned char*>(st) + C::BL)[f] =
-                    make_float4(lo_part2(x.x, x.y).x, lo_part2(x.x, x.y).y, lo_part2(x.z, x.w).x, lo_part2(x.z, x.w).y);
+                    for (int h = 0; h < 2; ++h) {
+                        const float4 x = src[h];
+                        const float2 l01 = lo_part2(x.x, x.y), l23 = lo_part2(x.z, x.w);
+                        dst[h] = make_float4(l01.x, l01.y, l23.x, l23.y);
+                    }
+                }
+            } else {
+                // B_lo, elementwise at the same swizzled offsets
+#pragma unroll
+                for (uint32_t f = t; f < QS * (C::SL / 16); f += TM) {
+                    const float4 x = reinterpret_cast<const float4*>(st + C::BH)[f];
+                    const float2 l01 = lo_part2(x.x, x.y), l23 = lo_part2(x.z, x.w);
+                    reinterpret_cast<float4*>(const_cast<unsigned char*>(st) + C::BL)[f] =
+                        make_float4(l01.x, l01.y, l23.x, l23.y);
+                }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -890,14 +907,15 @@ __global__ void __launch_bounds__(TN_THREADS + 32, 1) k6_gemm_tn_tc(const __grid
             const uint32_t last = nb - 1;
             mbar_wait(smem_u32(&lofree[last % LOB]), (last / LOB) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;");
-            float acc[64 * QS];
+            constexpr int HALF = (int)C::ND / 2;
+            float acc[C::ND];
 #pragma unroll
-            for (int c = 0; c < 64 * QS; c += 16) tmem_ld16(tmem + lane_off + (uint32_t)c, acc + c);
+            for (int c = 0; c < (int)C::ND; c += 16) tmem_ld16(tmem + lane_off + (uint32_t)c, acc + c);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (t < g.p) {
 #pragma unroll
-                for (int j = 0; j < 32 * QS; ++j)
-                    if ((uint32_t)j < g.q) out[t * g.q + j] = acc[j] + acc[32 * QS + j];
+                for (int j = 0; j < HALF; ++j)
+                    if ((uint32_t)j < g.q) out[t * g.q + j] = acc[j] + acc[HALF + j];
             }
         }
     }
@@ -929,21 +947,22 @@ bool make_map(CUtensorMap* map, const float* ptr, uint32_t cols, uint32_t rows, 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int PS, int QS>
+template <int PS, int QS, int BK>
 bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uint32_t p, uint32_t q, float* out) {
     CUtensorMap amap, bmap;
-    if (!make_map(&amap, a, p, m, TN_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
-        !make_map(&bmap, b, q, m, TN_BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    if (!make_map(&amap, a, p, m, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+        !make_map(&bmap, b, q, m, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
         return false;
-    using C = TnCfg<PS, QS>;
+    using C = TnCfg<PS, QS, BK>;
+    {
     static const bool prod = [] {
         const char* e = std::getenv("GNNA_TN_PROD");  // A/B switch (0: the MMA warp refills)
         return !(e && *e == '0');
     }();
-    auto kern = prod ? k6_gemm_tn_tc<PS, QS, true> : k6_gemm_tn_tc<PS, QS, false>;
+    auto kern = prod ? k6_gemm_tn_tc<PS, QS, BK, true> : k6_gemm_tn_tc<PS, QS, BK, false>;
     static std::atomic<uint64_t> attr{0};
     smem_attr_once(attr, kern, ctx->device, C::SMEM);
-    const uint32_t nblk = (m + TN_BK - 1) / TN_BK;
+    const uint32_t nblk = (m + BK - 1) / BK;
     uint32_t ctas = nblk < (uint32_t)ctx->num_sms ? nblk : (uint32_t)ctx->num_sms;
     const uint32_t bpc = (nblk + ctas - 1) / ctas;
     ctas = (nblk + bpc - 1) / bpc;
@@ -961,6 +980,7 @@ bool launch_tn_tc(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uin
         launched(ctx, "k_reduce_partials");
     }
     return true;
+    }
 }
 
 }  // namespace
@@ -993,6 +1013,19 @@ bool gemm_tc_f32(gnna_ctx* ctx, const float* a, const float* w, const float* bia
     return true;
 }
 
+namespace {
+template <int PS, int QS>
+bool launch_tn_bk(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, uint32_t p, uint32_t q, float* out) {
+    static const bool big = [] {
+        const char* e = std::getenv("GNNA_TN_BK");  // A/B switch (64: always 64-row blocks)
+        return !(e && std::atoi(e) == 64);
+    }();
+    if constexpr (TnCfg<PS, QS, 128>::S >= 3)
+        if (big) return launch_tn_tc<PS, QS, 128>(ctx, a, b, m, p, q, out);
+    return launch_tn_tc<PS, QS, 64>(ctx, a, b, m, p, q, out);
+}
+}  // namespace
+
 // out(p x q) = a(m x p)^T b(m x q) on tcgen05.  Returns false (nothing
 // launched) unless p, q are multiples of 4 (TMA row pitch), p <= 128, q <= 64
 // and both operands are 16-byte aligned.
@@ -1005,12 +1038,17 @@ bool gemm_tn_tc_f32(gnna_ctx* ctx, const float* a, const float* b, uint32_t m, u
     auto go = [&](auto qs) {
         constexpr int QS = decltype(qs)::value;
         switch (ps) {
-            case 1: return launch_tn_tc<1, QS>(ctx, a, b, m, p, q, out);
-            case 2: return launch_tn_tc<2, QS>(ctx, a, b, m, p, q, out);
-            case 3: return launch_tn_tc<3, QS>(ctx, a, b, m, p, q, out);
-            default: return launch_tn_tc<4, QS>(ctx, a, b, m, p, q, out);
+            case 1: return launch_tn_bk<1, QS>(ctx, a, b, m, p, q, out);
+            case 2: return launch_tn_bk<2, QS>(ctx, a, b, m, p, q, out);
+            case 3: return launch_tn_bk<3, QS>(ctx, a, b, m, p, q, out);
+            default: return launch_tn_bk<4, QS>(ctx, a, b, m, p, q, out);
         }
     };
+    static const bool pack = [] {
+        const char* e = std::getenv("GNNA_TN_PACK");  // A/B switch (0: separate B_lo slice)
+        return !(e && *e == '0');
+    }();
+    if (q <= 16 && pack) return go(std::integral_constant<int, 0>{});
     return q <= 32 ? go(std::integral_constant<int, 1>{}) : go(std::integral_constant<int, 2>{});
 }
 

@@ -16,12 +16,15 @@ __device__ __forceinline__ void wait(uint32_t bar, uint32_t ph) {
     asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(bar), "r"(ph) : "memory");
 }
 
-template <int R, int S, bool D3>
-__global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap map, uint32_t nblk, uint32_t bpc, unsigned long long* sink) {
+template <int R, int S, bool D3, int BM = 0>
+__global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap bmap,
+                                           uint32_t nblk, uint32_t bpc, unsigned long long* sink, const float* bsrc) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint64_t full[S], empty[S];
     const uint32_t base = (su32(sm) + 1023u) & ~1023u;
-    constexpr uint32_t SLB = R * 128, ST = 3 * SLB;
+    // BM: 0 = A only; 1 = + one {32, R} box of a 16-wide B (half out of bounds);
+    // 2 = + one 1-D bulk copy of the R x 64-byte B rows
+    constexpr uint32_t SLB = R * 128, ST = 3 * SLB + (BM ? SLB : 0), TX = 3 * SLB + (BM == 1 ? SLB : BM == 2 ? R * 64 : 0);
     const uint32_t b0 = blockIdx.x * bpc;
     const uint32_t nb = b0 >= nblk ? 0 : (nblk - b0 < bpc ? nblk - b0 : bpc);
     if (threadIdx.x == 0) {
@@ -34,7 +37,13 @@ __global__ void __launch_bounds__(64, 1) k(const __grid_constant__ CUtensorMap m
     __syncthreads();
     auto issue = [&](uint32_t i) {
         const uint32_t s = i % S, row = (b0 + i) * R, bar = su32(&full[s]), st = base + s * ST;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(ST) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(TX) : "memory");
+        if (BM == 1)
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         ::"r"(st + 3 * SLB), "l"((uint64_t)&bmap), "r"(0), "r"(row), "r"(bar) : "memory");
+        if (BM == 2)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(st + 3 * SLB), "l"(bsrc + (size_t)row * 16), "r"(R * 64), "r"(bar) : "memory");
         if (D3) {
             asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                          ::"r"(st), "l"((uint64_t)&map), "r"(0), "r"(row), "r"(0), "r"(bar) : "memory");
@@ -64,9 +73,17 @@ typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, co
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                         CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <int R, int S, bool D3>
-void run(Enc enc, float* x, uint64_t m, int sms, unsigned long long* sink) {
-    CUtensorMap map;
+template <int R, int S, bool D3, int BM = 0>
+void run(Enc enc, float* x, uint64_t m, int sms, unsigned long long* sink, float* bx = nullptr) {
+    CUtensorMap map, bmap{};
+    if (BM == 1) {
+        const cuuint64_t dims[2] = {16, m};
+        const cuuint64_t strides[1] = {16 * 4};
+        const cuuint32_t box[2] = {32, R};
+        const cuuint32_t es2[2] = {1, 1};
+        enc(&bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, bx, dims, strides, box, es2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     CUresult rc;
     const cuuint32_t es[3] = {1, 1, 1};
     if (D3) {
@@ -83,25 +100,25 @@ void run(Enc enc, float* x, uint64_t m, int sms, unsigned long long* sink) {
                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (rc != CUDA_SUCCESS) { printf("{\"R\": %d, \"S\": %d, \"d3\": %d, \"encode_error\": %d}\n", R, S, (int)D3, (int)rc); return; }
-    const size_t smem = (size_t)S * 3 * R * 128 + 1024;
+    const size_t smem = (size_t)S * (3 + (BM ? 1 : 0)) * R * 128 + 1024;
     if (smem > 227 * 1024) return;
-    cudaFuncSetAttribute(k<R, S, D3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k<R, S, D3, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const uint32_t nblk = (uint32_t)(m / R), bpc = (nblk + sms - 1) / sms, ctas = (nblk + bpc - 1) / bpc;
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     float best = 1e30f;
     for (int rep = 0; rep < 6; ++rep) {
         cudaEventRecord(a);
-        k<R, S, D3><<<ctas, 64, smem>>>(map, nblk, bpc, sink);
+        k<R, S, D3, BM><<<ctas, 64, smem>>>(map, bmap, nblk, bpc, sink, bx);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms; cudaEventElapsedTime(&ms, a, b);
         if (rep) best = ms < best ? ms : best;
     }
     cudaError_t e = cudaGetLastError();
-    const double bytes = (double)nblk * R * 96 * 4;
-    printf("{\"R\": %d, \"S\": %d, \"d3\": %d, \"inflight_kb\": %d, \"ms\": %.4f, \"GBps\": %.1f, \"err\": \"%s\"}\n", R, S, (int)D3,
-           S * 3 * R * 128 / 1024, best, bytes / best / 1e6, cudaGetErrorString(e));
+    const double bytes = (double)nblk * R * (96 + (BM ? 16 : 0)) * 4;
+    printf("{\"R\": %d, \"S\": %d, \"d3\": %d, \"bm\": %d, \"inflight_kb\": %d, \"ms\": %.4f, \"GBps\": %.1f, \"err\": \"%s\"}\n", R, S, (int)D3,
+           BM, S * 3 * R * 128 / 1024, best, bytes / best / 1e6, cudaGetErrorString(e));
 }
 
 int main() {
@@ -112,6 +129,12 @@ int main() {
     const uint64_t m = 4u << 20;  // 4M rows x 96 f32 = 1.6 GB (>> L2)
     float* x; cudaMalloc(&x, m * 96 * 4); cudaMemset(x, 0, m * 96 * 4);
     unsigned long long* sink; cudaMalloc(&sink, 4096 * 8);
+    float* bx; cudaMalloc(&bx, m * 16 * 4); cudaMemset(bx, 0, m * 16 * 4);
+    run<64, 5, false, 0>(enc, x, m, sms, sink, bx);
+    run<64, 5, false, 1>(enc, x, m, sms, sink, bx);
+    run<64, 5, false, 2>(enc, x, m, sms, sink, bx);
+    run<64, 3, false, 1>(enc, x, m, sms, sink, bx);
+    run<64, 3, false, 2>(enc, x, m, sms, sink, bx);
     run<64, 2, false>(enc, x, m, sms, sink);
     run<64, 3, false>(enc, x, m, sms, sink);
     run<64, 5, false>(enc, x, m, sms, sink);

@@ -78,7 +78,7 @@ def test_gemm_tc_is_the_kernel_launched(ctx):
 
 TN_SHAPES = [(1, 4, 4), (31, 16, 16), (33, 96, 16), (1000, 96, 16), (5000, 16, 24), (4097, 64, 64), (2000, 128, 32),
              (777, 100, 60), (3000, 16, 22), (410236, 96, 16), (410236, 16, 22), (5000, 7, 13), (1, 3, 5),
-             (20000, 30, 22), (1000, 130, 6)]
+             (20000, 30, 22), (1000, 130, 6), (2000, 64, 8), (3000, 32, 12), (100000, 128, 16)]
 
 
 @pytest.mark.parametrize("m,p,q", TN_SHAPES)
