@@ -347,27 +347,25 @@ __global__ void __launch_bounds__(FL_ROWS) k6_gemm_flat(GemmArgs g) {
         __syncthreads();
         if (tile + gridDim.x < tiles) load(tile + gridDim.x);
         if (t < rows) {
-            float acc[NJ];
+            float2 acc[NJ / 2];  // column pairs on packed FFMA2 (per-lane fmaf: the same roundings)
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) acc[j] = 0.f;
+            for (int j = 0; j < NJ / 2; ++j) acc[j] = make_float2(0.f, 0.f);
             const float* ar = sa + t * kp;
 #pragma unroll 4
             for (uint32_t kk = 0; kk < k; ++kk) {
-                const float av = ar[kk];
+                const float2 av = make_float2(ar[kk], ar[kk]);
 #pragma unroll
                 for (int j = 0; j < NJ; j += 4) {
                     const float4 w4 = *reinterpret_cast<const float4*>(&sw[kk * NJ + j]);
-                    acc[j] = fmaf(av, w4.x, acc[j]);
-                    acc[j + 1] = fmaf(av, w4.y, acc[j + 1]);
-                    acc[j + 2] = fmaf(av, w4.z, acc[j + 2]);
-                    acc[j + 3] = fmaf(av, w4.w, acc[j + 3]);
+                    acc[j / 2] = __ffma2_rn(av, make_float2(w4.x, w4.y), acc[j / 2]);
+                    acc[j / 2 + 1] = __ffma2_rn(av, make_float2(w4.z, w4.w), acc[j / 2 + 1]);
                 }
             }
             const float s = g.epilogue == 2 ? (float)g.row_scale[row0 + t] : 1.f;
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 if (j >= (int)n) break;
-                float val = acc[j];
+                float val = j % 2 ? acc[j / 2].y : acc[j / 2].x;
                 if (g.epilogue == 1) {
                     val += static_cast<const float*>(g.bias)[j];
                     val = val > 0.f ? val : 0.f;
@@ -1075,12 +1073,13 @@ void launch_gemm(gnna_ctx* ctx, const GemmArgs& g, bool exact) {
     if (g.m == 0 || g.n == 0) return;
     if constexpr (std::is_same<T, float>::value) {
         if (!exact) {
-            static const bool no_flat = std::getenv("GNNA_GEMM_NOFLAT") != nullptr;  // A/B switch
+            static const bool no_flat = std::getenv("GNNA_GEMM_NOFLAT") != nullptr;  // A/B switches
+            static const bool all_flat = std::getenv("GNNA_GEMM_FLAT") != nullptr;
             // Only where the tcgen05 path cannot TMA-tile A (k % 4 != 0): in the
             // C3 train step the 22 -> 16 product takes 25.1 us here against 41.0
             // on tcgen05 with scalar A loads, while 16 -> 22 stays on TMA (22.9
             // us, flat 24.2; ncu, profiles/r01p_gemm_flat.md).
-            if (!no_flat && g.k <= (uint32_t)FL_K && g.n <= (uint32_t)FL_K && g.k % 4 != 0 &&
+            if (!no_flat && g.k <= (uint32_t)FL_K && g.n <= (uint32_t)FL_K && (g.k % 4 != 0 || all_flat) &&
                 (uintptr_t)g.a % 16 == 0 && (uintptr_t)g.out % 16 == 0) {
                 static const int per_sm = std::getenv("GNNA_FLAT_CTAS") ? std::atoi(std::getenv("GNNA_FLAT_CTAS")) : 4;
                 const uint64_t tiles = (g.m + FL_ROWS - 1) / FL_ROWS;
