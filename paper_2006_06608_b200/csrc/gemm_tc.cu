@@ -574,6 +574,250 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
 }
 
+// The same product with the roles split (K 128; GNNA_TC_SPLIT=0/1 forces): warps
+// 0-3 only convert (A_lo into a LOB-deep TMEM ring), warps 4-7 only run the
+// epilogue (two TMEM accumulators), warp 8 issues the MMAs, warp 9 refills
+// the TMA ring as each stage's MMAs commit.  In the two-group kernel above a
+// group converts tile i + 2 only after its epilogue of tile i, so the tensor
+// pipe waited on epilogue + conversion every tile; here conversion runs up to
+// LOB tiles ahead and the epilogue trails.  It wins only where conversion is
+// heavy (K 128): with 4 converter warps instead of 8 the narrower products
+// convert too slowly, and every tile's MMAs are bound by shared-memory reads
+// (tensor-core A reads + TMA writes + converter loads, ~128 B/cycle; a clock64
+// trace showed 24 MMAs taking ~1,600 cycles per 128-row tile at C3).
+constexpr int TCS_THREADS = 2 * TM + 64;
+
+template <int KP, int NP>
+struct TcSplitCfg {
+    using C = TmaCfg<KP, NP>;
+    static constexpr uint32_t ACC = C::ACC;
+    static constexpr int LOB = 2 * ACC + 3 * KP <= 512 ? 3 : 2;
+    static constexpr uint32_t LO0 = 2 * ACC;
+    static constexpr uint32_t NEED = LO0 + LOB * KP;
+    static constexpr uint32_t TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
+    static_assert(NEED <= 512, "TMEM");
+};
+
+template <int KP, int NP>
+__global__ void __launch_bounds__(TCS_THREADS, 1)
+    k6_gemm_tc_tma_split(const __grid_constant__ CUtensorMap tmap, TcArgs g) {
+    using C = TmaCfg<KP, NP>;
+    using D = TcSplitCfg<KP, NP>;
+    constexpr int S = C::S, LOB = D::LOB;
+    static_assert(KP % 32 == 0 && S >= 2, "config");
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint64_t full[S], empty[S], lo_full[LOB], lo_free[LOB], acc_full[2], acc_free[2];
+    __shared__ uint32_t tmem_slot;
+    const uint32_t raw_a = smem_u32(smem_raw);
+    const uint32_t base = (raw_a + 1023u) & ~1023u;
+    unsigned char* base_p = smem_raw + (base - raw_a);
+    const uint32_t w_a = base + S * C::STAGE;
+    unsigned char* w_p = base_p + S * C::STAGE;
+    float* ostage = reinterpret_cast<float*>(w_p + C::WB);
+
+    const uint32_t t = threadIdx.x, warp = t / 32, lane = t % 32;
+    const uint32_t j0 = blockIdx.y * NP;
+    const uint32_t nj = g.n - j0 < (uint32_t)NP ? g.n - j0 : (uint32_t)NP;
+    const uint32_t my_tiles = g.tiles > blockIdx.x ? (g.tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    auto issue = [&](uint32_t i) {  // one thread: TMA of this CTA's i-th tile into stage i % S
+        const uint32_t s = i % S, tile = blockIdx.x + i * gridDim.x;
+        const uint32_t bar = smem_u32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(C::STAGE) : "memory");
+#pragma unroll
+        for (int sl = 0; sl < C::SL; ++sl)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(base + s * C::STAGE + sl * C::SLICE),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(sl * 32), "r"(tile * TM), "r"(bar)
+                : "memory");
+    };
+
+    if (t == 2 * TM) {  // MMA warp, lane 0: barriers, then the first S loads (overlap the W staging below)
+        for (int s = 0; s < S; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
+        }
+        for (int b = 0; b < LOB; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&lo_full[b])), "r"(TM));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&lo_free[b])));
+        }
+        for (int a = 0; a < 2; ++a) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&acc_full[a])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&acc_free[a])), "r"(TM));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        for (uint32_t i = 0; i < (uint32_t)S && i < my_tiles; ++i) issue(i);
+    }
+    if (t < 2 * TM) {
+        // [W_hi^T ; W_lo^T]: 2*NP rows, K-major, 128-byte swizzle (chunk ^= row % 8)
+        constexpr int PER = NP * KP / (2 * TM);
+        float wv[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const uint32_t e = t + q * 2 * TM, nn = e / KP, kk = e % KP;
+            wv[q] = (nn < nj && kk < g.k) ? __ldg(g.w + (uint64_t)kk * g.n + j0 + nn) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const uint32_t e = t + q * 2 * TM, nn = e / KP, kk = e % KP;
+            const float hi = rna_tf32(wv[q]), lo = rna_tf32(wv[q] - hi);
+            const uint32_t sl = kk / 32, c = (kk % 32) / 4, b = (kk % 4) * 4;
+            const uint32_t r0 = nn, r1 = NP + nn;
+            *reinterpret_cast<float*>(w_p + sl * C::WSL + (r0 / 8) * 1024 + (r0 % 8) * 128 + ((c ^ (r0 % 8)) * 16) +
+                                      b) = hi;
+            *reinterpret_cast<float*>(w_p + sl * C::WSL + (r1 / 8) * 1024 + (r1 % 8) * 128 + ((c ^ (r1 % 8)) * 16) +
+                                      b) = lo;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // W (generic stores) -> tensor core
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                     "r"(D::TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_slot;
+
+    if (warp == 8) {
+        constexpr uint32_t IDESC_2N = idesc_tf32<2 * NP>();
+        constexpr uint32_t IDESC_N = idesc_tf32<NP>();
+        for (uint32_t i = 0; i < my_tiles; ++i) {
+            const uint32_t s = i % S, b = i % LOB, a = i & 1u;
+            mbar_wait(smem_u32(&lo_full[b]), (i / LOB) & 1u);        // converters done (stage s has landed)
+            if (i >= 2) mbar_wait(smem_u32(&acc_free[a]), ((i - 2) >> 1) & 1u);  // epilogue read tile i - 2
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                const uint32_t a_hi = base + s * C::STAGE;
+                const uint32_t d = tmem + a * D::ACC, a_lo = tmem + D::LO0 + b * KP;
+#pragma unroll
+                for (int sl = 0; sl < C::SL; ++sl)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t ao = sl * C::SLICE + q * 32, bo = sl * C::WSL + q * 32;
+                        mma_tf32(d, smem_desc_sw128(a_hi + ao), smem_desc_sw128(w_a + bo), IDESC_2N,
+                                 (sl | q) ? 1u : 0u);
+                        mma_tf32_ts(d, a_lo + sl * 32 + q * 8, smem_desc_sw128(w_a + bo), IDESC_N, 1u);
+                    }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&acc_full[a]))
+                             : "memory");
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&lo_free[b]))
+                             : "memory");
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 smem_u32(&empty[s]))
+                             : "memory");
+            }
+            __syncwarp();
+        }
+    } else if (warp == 9) {
+        if (lane == 0)
+            for (uint32_t i = S; i < my_tiles; ++i) {
+                mbar_wait(smem_u32(&empty[(i - S) % S]), ((i - S) / S) & 1u);
+                issue(i);
+            }
+    } else if (warp < 4) {
+        // converters: thread r = TMEM lane r = tile row r
+        const uint32_t lane_off = (warp * 32u) << 16;
+        const uint32_t r = warp * 32 + lane, r8 = r % 8;
+        const uint32_t row_off = (r / 8) * 1024 + r8 * 128;
+        for (uint32_t i = 0; i < my_tiles; ++i) {
+            const uint32_t s = i % S, b = i % LOB;
+            mbar_wait(smem_u32(&full[s]), (i / S) & 1u);
+            if (i >= (uint32_t)LOB) mbar_wait(smem_u32(&lo_free[b]), ((i - LOB) / LOB) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const unsigned char* stg = base_p + s * C::STAGE + row_off;
+#pragma unroll
+            for (int sl = 0; sl < C::SL; ++sl) {
+                float4 x[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    x[c] = *reinterpret_cast<const float4*>(stg + sl * C::SLICE + ((c ^ r8) * 16));
+                float lo[32];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float2 l01 = lo_part2(x[c].x, x[c].y), l23 = lo_part2(x[c].z, x[c].w);
+                    lo[4 * c] = l01.x, lo[4 * c + 1] = l01.y, lo[4 * c + 2] = l23.x, lo[4 * c + 3] = l23.y;
+                }
+                const uint32_t col = tmem + lane_off + D::LO0 + b * KP + sl * 32;
+                tmem_st16(col, lo);
+                tmem_st16(col + 16, lo + 16);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lo_full[b])) : "memory");
+        }
+    } else {
+        // epilogue warps 4-7: thread = TMEM lane (warp - 4) * 32 + lane = tile row
+        const uint32_t wq = warp - 4;
+        const uint32_t lane_off = (wq * 32u) << 16;
+        for (uint32_t i = 0; i < my_tiles; ++i) {
+            const uint32_t a = i & 1u;
+            mbar_wait(smem_u32(&acc_full[a]), (i >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            float acc[2 * NP];
+#pragma unroll
+            for (int c = 0; c < 2 * NP; c += 16) tmem_ld16(tmem + lane_off + a * D::ACC + (uint32_t)c, acc + c);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&acc_free[a])) : "memory");
+#pragma unroll
+            for (int q = 0; q < NP; ++q) acc[q] += acc[NP + q];
+            const uint64_t row0 = (uint64_t)(blockIdx.x + i * gridDim.x) * TM + wq * 32;
+            const uint64_t row = row0 + lane;
+            if (row < g.m) {
+                if (g.epilogue == 1) {
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const float x = acc[q] + ((uint32_t)q < nj ? __ldg(g.bias + j0 + q) : 0.f);
+                        acc[q] = x > 0.f ? x : 0.f;
+                    }
+                } else if (g.epilogue == 2) {
+                    const float sc = (float)g.row_scale[row];
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) acc[q] *= sc;
+                }
+            }
+            if (gridDim.y == 1) {
+                float* st = ostage + wq * 32 * C::OSTRIDE;
+#pragma unroll
+                for (int q = 0; q < NP; ++q) st[lane * C::OSTRIDE + q] = acc[q];
+                __syncwarp();
+                const uint32_t rows = row0 >= g.m ? 0u : (g.m - row0 < 32u ? (uint32_t)(g.m - row0) : 32u);
+                const uint32_t total = rows * g.n;
+                float* o = g.out + row0 * g.n;
+                uint32_t rr = lane / g.n, cc = lane % g.n;
+                const uint32_t dr = 32u / g.n, dc = 32u % g.n;
+                for (uint32_t e = lane; e < total; e += 32) {
+                    o[e] = st[rr * C::OSTRIDE + cc];
+                    rr += dr, cc += dc;
+                    if (cc >= g.n) cc -= g.n, ++rr;
+                }
+                __syncwarp();
+            } else if (row < g.m) {
+                float* o = g.out + row * g.n + j0;
+                if (nj == (uint32_t)NP && g.n % 4 == 0 && ((uintptr_t)o % 16 == 0)) {
+#pragma unroll
+                    for (int q = 0; q < NP; q += 4)
+                        *reinterpret_cast<float4*>(o + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NP; ++q)
+                        if ((uint32_t)q < nj) o[q] = acc[q];
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(D::TCOLS));
+}
+
 // cudaFuncSetAttribute is per device: each kernel instance remembers the
 // devices it was configured on (one bit per device ordinal).
 template <class K>
@@ -610,13 +854,20 @@ bool launch_tc_tma(gnna_ctx* ctx, const TcArgs& g) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     using C = TmaCfg<KP, NP>;
-    auto kern = k6_gemm_tc_tma<KP, NP>;
+    // split roles where conversion is heavy (K 128: 143 -> 93 us at 410k x 128 -> 64);
+    // the two-group kernel elsewhere (C3 96 -> 16: 34.3 vs 37.2 us, 16 -> 22: 21.8 vs 26.2)
+    static const int split_env = [] {
+        const char* e = std::getenv("GNNA_TC_SPLIT");  // A/B switch: 0 / 1 force either kernel
+        return e && *e ? std::atoi(e) : -1;
+    }();
+    const bool split = split_env >= 0 ? split_env != 0 : KP >= 128;
+    auto kern = split ? k6_gemm_tc_tma_split<KP, NP> : k6_gemm_tc_tma<KP, NP>;
     static std::atomic<uint64_t> attr{0};
     smem_attr_once(attr, kern, ctx->device, C::SMEM);
     const uint32_t cols = (g.n + NP - 1) / NP;
     const uint32_t slots = (uint32_t)ctx->num_sms / cols;
     dim3 grid(g.tiles < slots ? g.tiles : (slots ? slots : 1), cols);
-    kern<<<grid, TC_THREADS, C::SMEM, ctx->stream>>>(map, g);
+    kern<<<grid, split ? TCS_THREADS : TC_THREADS, C::SMEM, ctx->stream>>>(map, g);
     launched(ctx, "k6_gemm_tc_tma");
     return true;
 }

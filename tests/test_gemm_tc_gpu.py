@@ -124,3 +124,37 @@ def test_gemm_flat_narrow_epilogues(ctx, m, k, n):
     flat = torch.zeros(m * k + 1, dtype=torch.float32, device="cuda")
     flat[1:] = da.reshape(-1)
     check(ctx.gemm(flat[1:].view(m, k), dw).cpu().numpy(), a64, w64)
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_gemm_tc_both_kernels(split):
+    """Both X·W kernels (two converter/epilogue groups, and the split-role one
+    the K 128 shapes take) on shapes of either default, with both epilogues:
+    GNNA_TC_SPLIT forces one (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2006_06608_b200.capi import Context
+from test_gemm_tc_gpu import check
+ctx = Context(0)
+rng = np.random.default_rng(9)
+for m, k, n in [(4096, 96, 16), (410, 16, 22), (3001, 128, 64), (513, 100, 130)]:
+    a = (rng.random((m, k)) - 0.5).astype(np.float32)
+    w = (rng.random((k, n)) - 0.5).astype(np.float32)
+    b = (rng.random(n) - 0.5).astype(np.float32)
+    s = rng.random(m)
+    da, dw, db, ds = (torch.from_numpy(v).cuda() for v in (a, w, b, s))
+    a64, w64, b64 = a.astype(np.float64), w.astype(np.float64), b.astype(np.float64)
+    check(ctx.gemm(da, dw).cpu().numpy(), a64, w64)
+    check(ctx.gemm(da, dw, db, 1).cpu().numpy(), a64, w64,
+          lambda x, bd: (np.maximum(x + b64, 0), bd + np.abs(b64)))
+    check(ctx.gemm(da, dw, None, 2, ds).cpu().numpy(), a64, w64, lambda x, bd: (x * s[:, None], bd * s[:, None]))
+print("ok")
+'''
+    r = subprocess.run([sys.executable, "-c", code, ROOT], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, GNNA_TC_SPLIT=split))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
