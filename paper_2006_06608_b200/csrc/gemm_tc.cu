@@ -313,6 +313,10 @@ struct TmaCfg {
     static constexpr uint32_t NEED = LO0 + 2 * KP;
     static constexpr uint32_t TCOLS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128 : NEED <= 256 ? 256 : 512;
     static_assert(NEED <= 512, "TMEM");
+    // AT: the converters also store A_hi (the raw tile) into TMEM and both MMAs
+    // are TS, so the tensor core reads only W from shared memory
+    static constexpr bool AT_FITS = LO0 + 4 * KP <= 512;
+    static constexpr uint32_t TCOLS_AT = AT_FITS ? (LO0 + 4 * KP <= 256 ? 256 : 512) : 512;
 };
 
 __device__ __forceinline__ float trunc_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
@@ -367,11 +371,13 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 constexpr int TC_CONV = 2 * TM;
 constexpr int TC_THREADS = TC_CONV + 32;
 
-template <int KP, int NP>
+template <int KP, int NP, bool AT>
 __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_constant__ CUtensorMap tmap, TcArgs g) {
     using C = TmaCfg<KP, NP>;
     constexpr int S = C::S;
-    static_assert(KP % 32 == 0 && S >= 2, "config");
+    static_assert(KP % 32 == 0 && S >= 2 && (!AT || C::AT_FITS), "config");
+    constexpr uint32_t TCOLS = AT ? C::TCOLS_AT : C::TCOLS;
+    constexpr uint32_t LOB_COLS = AT ? 2 * KP : KP;  // per buffer: A_lo [| A_hi]
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint64_t full[S];
     __shared__ uint64_t lo_full[2];
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                     "r"(C::TCOLS));
+                     "r"(TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -455,14 +461,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
             asm volatile("tcgen05.fence::after_thread_sync;");
             if (lane == 0) {
                 const uint32_t a_hi = base + s * C::STAGE;
-                const uint32_t d = tmem + b * C::ACC, a_lo = tmem + C::LO0 + b * KP;
+                const uint32_t d = tmem + b * C::ACC, a_lo = tmem + C::LO0 + b * LOB_COLS;
 #pragma unroll
                 for (int sl = 0; sl < C::SL; ++sl)
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         const uint32_t ao = sl * C::SLICE + q * 32, bo = sl * C::WSL + q * 32;
-                        mma_tf32(d, smem_desc_sw128(a_hi + ao), smem_desc_sw128(w_a + bo), IDESC_2N,
-                                 (sl | q) ? 1u : 0u);
+                        if (AT)
+                            mma_tf32_ts(d, a_lo + KP + sl * 32 + q * 8, smem_desc_sw128(w_a + bo), IDESC_2N,
+                                        (sl | q) ? 1u : 0u);
+                        else
+                            mma_tf32(d, smem_desc_sw128(a_hi + ao), smem_desc_sw128(w_a + bo), IDESC_2N,
+                                     (sl | q) ? 1u : 0u);
                         mma_tf32_ts(d, a_lo + sl * 32 + q * 8, smem_desc_sw128(w_a + bo), IDESC_N, 1u);
                     }
                 asm volatile(
@@ -503,9 +513,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
                         const float2 l01 = lo_part2(x[c].x, x[c].y), l23 = lo_part2(x[c].z, x[c].w);
                         lo[4 * c] = l01.x, lo[4 * c + 1] = l01.y, lo[4 * c + 2] = l23.x, lo[4 * c + 3] = l23.y;
                     }
-                    const uint32_t col = tmem + lane_off + C::LO0 + b * KP + sl * 32;
+                    const uint32_t col = tmem + lane_off + C::LO0 + b * LOB_COLS + sl * 32;
                     tmem_st16(col, lo);
                     tmem_st16(col + 16, lo + 16);
+                    if (AT) {
+                        tmem_st16(col + KP, reinterpret_cast<const float*>(x));
+                        tmem_st16(col + KP + 16, reinterpret_cast<const float*>(x) + 16);
+                    }
                 }
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 asm volatile("tcgen05.fence::before_thread_sync;");
@@ -571,7 +585,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
     }
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TCOLS));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
 // The same product with the roles split (K 128; GNNA_TC_SPLIT=0/1 forces): warps
@@ -861,7 +875,12 @@ bool launch_tc_tma(gnna_ctx* ctx, const TcArgs& g) {
         return e && *e ? std::atoi(e) : -1;
     }();
     const bool split = split_env >= 0 ? split_env != 0 : KP >= 128;
-    auto kern = split ? k6_gemm_tc_tma_split<KP, NP> : k6_gemm_tc_tma<KP, NP>;
+    static const bool at_on = [] {
+        const char* e = std::getenv("GNNA_TC_AT");  // A/B switch (0: A_hi read from shared memory)
+        return !(e && *e == '0');
+    }();
+    auto kern = split ? k6_gemm_tc_tma_split<KP, NP>
+                      : (C::AT_FITS && at_on) ? k6_gemm_tc_tma<KP, NP, C::AT_FITS> : k6_gemm_tc_tma<KP, NP, false>;
     static std::atomic<uint64_t> attr{0};
     smem_attr_once(attr, kern, ctx->device, C::SMEM);
     const uint32_t cols = (g.n + NP - 1) / NP;
