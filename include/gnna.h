@@ -95,7 +95,11 @@ GNNA_API uint64_t gnna_launch_count(const gnna_ctx* ctx);
 
 /* Device memory for hosts that do not link the CUDA runtime themselves (the
  * gnnsim:: C++ drop-in).  Allocation is stream-ordered on ctx's stream;
- * gnna_copy_to_host synchronises the stream before returning. */
+ * gnna_copy_to_host synchronises the stream before returning.  Host buffers
+ * may be pageable: copies of 4 MiB and more from / to pageable memory go
+ * through the context's pinned bounce buffers (8 MiB chunks, host threads
+ * copying one chunk while the DMA engine moves the previous one); the host
+ * source of gnna_copy_to_device is free again when it returns. */
 GNNA_API gnna_status gnna_device_alloc(gnna_ctx* ctx, size_t bytes, void** out);
 GNNA_API gnna_status gnna_device_free(gnna_ctx* ctx, void* p);
 GNNA_API gnna_status gnna_copy_to_device(gnna_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);

@@ -1,10 +1,181 @@
 // Context lifecycle and the host-buffer end-to-end entry of include/gnna.h.
 #include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
 
 #include "gnna_common.cuh"
 
 namespace gnna {
+
+// ------------------------------------------------ pageable host transfers
+// cudaMemcpy from pageable memory is staged by the driver through its own
+// pinned buffer on one thread (~11 GB/s here).  Large pageable copies go
+// through the context's ring of pinned chunks instead: host threads copy
+// chunk k + 1 into its bounce buffer while the DMA engine moves chunk k.
+// Pinned (registered) host memory is copied directly, as before.
+struct HostPool {
+    explicit HostPool(unsigned n) : n_(n) {
+        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    unsigned size() const { return n_; }
+    // f(worker) on every worker; returns when all are done
+    void run(const std::function<void(unsigned)>& f) {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            job_ = &f;
+            pending_ = n_;
+            ++gen_;
+        }
+        cv_.notify_all();
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [&] { return pending_ == 0; });
+    }
+
+private:
+    void loop(unsigned i) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(unsigned)>* f;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                f = job_;
+            }
+            (*f)(i);
+            std::lock_guard<std::mutex> l(m_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    unsigned n_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(unsigned)>* job_ = nullptr;
+    uint64_t gen_ = 0;
+    unsigned pending_ = 0;
+    bool stop_ = false;
+};
+
+struct Staging {
+    static constexpr size_t CH = 8u << 20;  // bytes per bounce buffer
+    static constexpr int SLOTS = 3;
+    void* buf[SLOTS] = {};
+    cudaEvent_t ev[SLOTS] = {};
+    bool busy[SLOTS] = {};
+    HostPool pool;
+    explicit Staging(unsigned threads) : pool(threads) {
+        for (int i = 0; i < SLOTS; ++i) {
+            GNNA_CUDA(cudaHostAlloc(&buf[i], CH, cudaHostAllocDefault));
+            GNNA_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+    }
+    ~Staging() {
+        for (int i = 0; i < SLOTS; ++i) {
+            if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+            if (buf[i]) cudaFreeHost(buf[i]);
+        }
+    }
+    // memcpy split over the pool's threads in 64-byte aligned parts
+    void pmemcpy(void* dst, const void* src, size_t len) {
+        const unsigned n = pool.size();
+        const size_t part = ((len + n - 1) / n + 63) & ~size_t(63);
+        pool.run([&](unsigned i) {
+            const size_t b = (size_t)i * part;
+            if (b < len)
+                std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, std::min(part, len - b));
+        });
+    }
+};
+
+constexpr size_t kStageMin = 4u << 20;  // smaller copies: the driver's own staging
+
+bool pageable(const void* p) {
+    static const bool off = [] {
+        const char* e = std::getenv("GNNA_STAGING");  // A/B switch (0: the driver's staging)
+        return e && *e == '0';
+    }();
+    if (off) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+Staging& staging(gnna_ctx* ctx) {
+    if (!ctx->staging) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        ctx->staging = new Staging(std::min(8u, hw));
+    }
+    return *ctx->staging;
+}
+
+// Host -> device, stream-ordered on ctx->stream; the host source may be
+// reused as soon as this returns.
+void copy_h2d(gnna_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
+    if (!bytes) return;
+    if (bytes < kStageMin || !pageable(h_src)) {
+        // (a pageable source is free again on return: the driver stages it before returning)
+        GNNA_CUDA(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        return;
+    }
+    Staging& st = staging(ctx);
+    for (size_t off = 0, k = 0; off < bytes; off += Staging::CH, ++k) {
+        const int s = (int)(k % Staging::SLOTS);
+        const size_t len = std::min(Staging::CH, bytes - off);
+        if (st.busy[s]) GNNA_CUDA(cudaEventSynchronize(st.ev[s]));
+        st.pmemcpy(st.buf[s], static_cast<const char*>(h_src) + off, len);
+        GNNA_CUDA(cudaMemcpyAsync(static_cast<char*>(d_dst) + off, st.buf[s], len, cudaMemcpyHostToDevice, ctx->stream));
+        GNNA_CUDA(cudaEventRecord(st.ev[s], ctx->stream));
+        st.busy[s] = true;
+    }
+}
+
+// Device -> host after the work already queued on ctx->stream; returns when
+// the host buffer holds the data.
+void copy_d2h(gnna_ctx* ctx, void* h_dst, const void* d_src, size_t bytes) {
+    if (bytes < kStageMin || !pageable(h_dst)) {
+        if (bytes) GNNA_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+        GNNA_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
+    Staging& st = staging(ctx);
+    const size_t chunks = (bytes + Staging::CH - 1) / Staging::CH;
+    auto dma = [&](size_t k) {
+        const int s = (int)(k % Staging::SLOTS);
+        const size_t off = k * Staging::CH, len = std::min(Staging::CH, bytes - off);
+        if (st.busy[s]) GNNA_CUDA(cudaEventSynchronize(st.ev[s]));
+        GNNA_CUDA(cudaMemcpyAsync(st.buf[s], static_cast<const char*>(d_src) + off, len, cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+        GNNA_CUDA(cudaEventRecord(st.ev[s], ctx->stream));
+        st.busy[s] = true;
+    };
+    for (size_t k = 0; k < chunks && k < (size_t)Staging::SLOTS; ++k) dma(k);
+    for (size_t k = 0; k < chunks; ++k) {
+        const int s = (int)(k % Staging::SLOTS);
+        const size_t off = k * Staging::CH, len = std::min(Staging::CH, bytes - off);
+        GNNA_CUDA(cudaEventSynchronize(st.ev[s]));
+        st.pmemcpy(static_cast<char*>(h_dst) + off, st.buf[s], len);
+        st.busy[s] = false;
+        if (k + Staging::SLOTS < chunks) dma(k + Staging::SLOTS);
+    }
+}
+
 void validate_params(const gnna_params* p);
 void aggregate_plan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode, const void* x, void* y,
                     uint32_t epi, const float* scale, double alpha);
@@ -49,6 +220,17 @@ gnna_status gnna_create(int device, gnna_ctx** out) {
 }
 
 void gnna_destroy(gnna_ctx* ctx) { delete ctx; }
+
+}  // extern "C"
+
+gnna_ctx::~gnna_ctx() {
+    if (staging) {
+        cudaStreamSynchronize(stream);
+        delete staging;
+    }
+}
+
+extern "C" {
 
 gnna_status gnna_set_stream(gnna_ctx* ctx, void* stream) {
     return gnna::guard(ctx, [&] {
@@ -127,15 +309,14 @@ gnna_status gnna_device_free(gnna_ctx* ctx, void* p) {
 gnna_status gnna_copy_to_device(gnna_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
-        if (bytes) GNNA_CUDA(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        gnna::copy_h2d(ctx, d_dst, h_src, bytes);
     });
 }
 
 gnna_status gnna_copy_to_host(gnna_ctx* ctx, void* h_dst, const void* d_src, size_t bytes) {
     return gnna::guard(ctx, [&] {
         gnna::require_ctx(ctx);
-        if (bytes) GNNA_CUDA(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-        GNNA_CUDA(cudaStreamSynchronize(ctx->stream));
+        gnna::copy_d2h(ctx, h_dst, d_src, bytes);
     });
 }
 
@@ -162,16 +343,15 @@ gnna_status gnna_aggregate_host_rows(gnna_ctx* ctx, int dtype, const uint64_t* h
         gnna::DevBuf<uint8_t> x(xbytes ? xbytes : 1, s), y(ybytes ? ybytes : 1, s);
         GNNA_CUDA(cudaMemcpyAsync(rp.get(), h_row_ptr + row_begin, ((size_t)rows + 1) * 8, cudaMemcpyHostToDevice, s));
         if (e0) gnna::rebase_u64(ctx, rp.get(), (uint64_t)rows + 1, e0);
-        if (nnz) GNNA_CUDA(cudaMemcpyAsync(col.get(), h_col + e0, nnz * 4, cudaMemcpyHostToDevice, s));
-        if (xbytes) GNNA_CUDA(cudaMemcpyAsync(x.get(), h_x, xbytes, cudaMemcpyHostToDevice, s));
+        gnna::copy_h2d(ctx, col.get(), h_col + e0, nnz * 4);
+        gnna::copy_h2d(ctx, x.get(), h_x, xbytes);
         gnna_plan* plan = nullptr;
         gnna_status st = gnna_plan_create(ctx, rp.get(), col.get(), rows, 0, rows, p, strategy, &plan);
         if (st != GNNA_OK) gnna::raise(st, ctx->err);
         try {
             gnna::aggregate_plan(ctx, plan, dtype, dim_mode, x.get(), y.get(), 0, nullptr, 0.0);
             if (cost) gnna::cost_report(ctx, plan, dim_mode, line_bytes, cache_capacity, cache_line, cost);
-            if (ybytes) GNNA_CUDA(cudaMemcpyAsync(h_y, y.get(), ybytes, cudaMemcpyDeviceToHost, s));
-            GNNA_CUDA(cudaStreamSynchronize(s));
+            gnna::copy_d2h(ctx, h_y, y.get(), ybytes);
         } catch (...) {
             gnna_plan_destroy(plan);
             throw;

@@ -9,6 +9,10 @@
 
 #include "gnna.h"
 
+namespace gnna {
+struct Staging;  // pinned bounce buffers + host copy threads for pageable transfers (capi.cu)
+}
+
 struct gnna_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -17,6 +21,8 @@ struct gnna_ctx {
     int num_sms = 148;
     int l2_bytes = 0;
     int smem_optin = 0;
+    gnna::Staging* staging = nullptr;  // created on the first large pageable copy
+    ~gnna_ctx();
 };
 
 namespace gnna {

@@ -267,3 +267,27 @@ def test_capi_argument_checks(ctx, orc):
         plan.aggregate_ex(x, row_scale=torch.ones(299, device="cuda"))
     y = plan.aggregate_ex(x)  # aggregate_ex takes any width
     assert y.shape == x.shape
+
+
+@pytest.mark.parametrize("nbytes", [1000, (4 << 20) - 4, 4 << 20, (21 << 20) + 12, 64 << 20])
+def test_pageable_copies_staged(ctx, nbytes):
+    """gnna_copy_to_device / gnna_copy_to_host with PAGEABLE host buffers:
+    below 4 MiB the driver's own staging, from 4 MiB the context's pinned
+    bounce ring (8 MiB chunks, threaded host copies, partial last chunk).
+    Byte-exact round trip, through a device buffer the test also fills and
+    reads with torch; the source may be overwritten as soon as the upload
+    returns."""
+    import ctypes as C
+    rng = np.random.default_rng(nbytes)
+    src = rng.integers(0, 256, nbytes, dtype=np.uint8)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    L = ctx.L
+    ctx._check(L.gnna_copy_to_device(ctx.h, C.c_void_p(d.data_ptr()), C.c_void_p(src.ctypes.data), C.c_size_t(nbytes)))
+    keep = src.copy()
+    src[:] = 7  # the upload must not read the source after returning
+    ctx.synchronize()
+    assert np.array_equal(d.cpu().numpy(), keep)
+    d2 = torch.from_numpy(rng.integers(0, 256, nbytes, dtype=np.uint8)).cuda()
+    out = np.empty(nbytes, np.uint8)
+    ctx._check(L.gnna_copy_to_host(ctx.h, C.c_void_p(out.ctypes.data), C.c_void_p(d2.data_ptr()), C.c_size_t(nbytes)))
+    assert np.array_equal(out, d2.cpu().numpy())
