@@ -588,18 +588,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k6_gemm_tc_tma(const __grid_con
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
 }
 
-// The same product with the roles split (K 128; GNNA_TC_SPLIT=0/1 forces): warps
-// 0-3 only convert (A_lo into a LOB-deep TMEM ring), warps 4-7 only run the
-// epilogue (two TMEM accumulators), warp 8 issues the MMAs, warp 9 refills
-// the TMA ring as each stage's MMAs commit.  In the two-group kernel above a
+// The same product with the roles split (K 128 or N blocks of 64; GNNA_TC_SPLIT=0/1 forces): warps
+// 0-3 only convert (A_lo into a LOB-deep TMEM ring), warps 4-11 only run the
+// epilogue (two groups, one per TMEM accumulator, alternate tiles), warp 12
+// issues the MMAs, warp 13 refills the TMA ring as each stage's MMAs commit.  In the two-group kernel above a
 // group converts tile i + 2 only after its epilogue of tile i, so the tensor
 // pipe waited on epilogue + conversion every tile; here conversion runs up to
-// LOB tiles ahead and the epilogue trails.  It wins only where conversion is
-// heavy (K 128): with 4 converter warps instead of 8 the narrower products
-// convert too slowly, and every tile's MMAs are bound by shared-memory reads
+// LOB tiles ahead and the epilogue trails.  It wins where conversion or the
+// epilogue is heavy (K 128, 64 output columns); on the narrow C3 products the
+// two-group kernel stays ahead, and every tile's MMAs are bound by shared-memory reads
 // (tensor-core A reads + TMA writes + converter loads, ~128 B/cycle; a clock64
 // trace showed 24 MMAs taking ~1,600 cycles per 128-row tile at C3).
-constexpr int TCS_THREADS = 2 * TM + 64;
+constexpr int TCS_THREADS = 3 * TM + 64;
 
 template <int KP, int NP>
 struct TcSplitCfg {
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
                 : "memory");
     };
 
-    if (t == 2 * TM) {  // MMA warp, lane 0: barriers, then the first S loads (overlap the W staging below)
+    if (t == 3 * TM) {  // MMA warp, lane 0: barriers, then the first S loads (overlap the W staging below)
         for (int s = 0; s < S; ++s) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[s])));
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_slot;
 
-    if (warp == 8) {
+    if (warp == 12) {
         constexpr uint32_t IDESC_2N = idesc_tf32<2 * NP>();
         constexpr uint32_t IDESC_N = idesc_tf32<NP>();
         for (uint32_t i = 0; i < my_tiles; ++i) {
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
             }
             __syncwarp();
         }
-    } else if (warp == 9) {
+    } else if (warp == 13) {
         if (lane == 0)
             for (uint32_t i = S; i < my_tiles; ++i) {
                 mbar_wait(smem_u32(&empty[(i - S) % S]), ((i - S) / S) & 1u);
@@ -766,10 +766,11 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&lo_full[b])) : "memory");
         }
     } else {
-        // epilogue warps 4-7: thread = TMEM lane (warp - 4) * 32 + lane = tile row
-        const uint32_t wq = warp - 4;
+        // epilogue: warps 4-7 take the even tiles (accumulator 0), warps 8-11
+        // the odd ones (accumulator 1); thread = TMEM lane (warp % 4) * 32 + lane = tile row
+        const uint32_t grp = (warp - 4) / 4, wq = warp % 4;
         const uint32_t lane_off = (wq * 32u) << 16;
-        for (uint32_t i = 0; i < my_tiles; ++i) {
+        for (uint32_t i = grp; i < my_tiles; i += 2) {
             const uint32_t a = i & 1u;
             mbar_wait(smem_u32(&acc_full[a]), (i >> 1) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -797,7 +798,7 @@ __global__ void __launch_bounds__(TCS_THREADS, 1)
                 }
             }
             if (gridDim.y == 1) {
-                float* st = ostage + wq * 32 * C::OSTRIDE;
+                float* st = ostage + (warp - 4) * 32 * C::OSTRIDE;
 #pragma unroll
                 for (int q = 0; q < NP; ++q) st[lane * C::OSTRIDE + q] = acc[q];
                 __syncwarp();
@@ -868,13 +869,14 @@ bool launch_tc_tma(gnna_ctx* ctx, const TcArgs& g) {
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
     using C = TmaCfg<KP, NP>;
-    // split roles where conversion is heavy (K 128: 143 -> 93 us at 410k x 128 -> 64);
-    // the two-group kernel elsewhere (C3 96 -> 16: 34.3 vs 37.2 us, 16 -> 22: 21.8 vs 26.2)
+    // split roles for K 128 or 64-column blocks (410k x 128 -> 64: 141 -> 94 us,
+    // 1M x 64 -> 64: 93.5 -> 87); the two-group kernel for the narrow C3
+    // products (96 -> 16: 33.3 vs 37.0 us, 16 -> 22: 21.6 vs 22.3)
     static const int split_env = [] {
         const char* e = std::getenv("GNNA_TC_SPLIT");  // A/B switch: 0 / 1 force either kernel
         return e && *e ? std::atoi(e) : -1;
     }();
-    const bool split = split_env >= 0 ? split_env != 0 : KP >= 128;
+    const bool split = split_env >= 0 ? split_env != 0 : (KP >= 128 || NP >= 64);
     static const bool at_on = [] {
         const char* e = std::getenv("GNNA_TC_AT");  // A/B switch (0: A_hi read from shared memory)
         return !(e && *e == '0');
