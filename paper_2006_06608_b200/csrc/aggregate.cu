@@ -124,6 +124,7 @@ struct AggArgs {
     const uint32_t* col;
     const void* x;
     void* y;
+    const void* xself;  // EPI_SELF reads x[v] here when set (x is then the pre-scaled gather source)
     void* carry;
     uint32_t dim, nvec, kpl;
     int seq;
@@ -190,7 +191,8 @@ __device__ __forceinline__ void store_final(const AggArgs& a, uint32_t v, uint32
         if (a.epi & EPI_SELF) {
             const T c = a.sw ? T(a.sw[v]) : T(a.alpha);
             if (c != T(0)) {
-                const Vec<T, VEC> xv = ldv<T, VEC>(static_cast<const T*>(a.x) + (size_t)v * a.dim + off);
+                const Vec<T, VEC> xv =
+                    ldv<T, VEC>(static_cast<const T*>(a.xself ? a.xself : a.x) + (size_t)v * a.dim + off);
                 vaxpy_rn(val, c, xv);
             }
         }
@@ -865,6 +867,25 @@ void launch_k4(gnna_ctx* ctx, AggArgs& a, const Shape& s) {
 
 }  // namespace
 
+// xs[u] = w[u] * x[u] for every row (the per-source weights of a weighted
+// gather applied once per row instead of once per edge).
+__global__ void k_prescale_rows(const float* __restrict__ x, const float* __restrict__ w, uint32_t n, uint32_t dim,
+                                float* __restrict__ xs) {
+    const uint64_t total = (uint64_t)n * dim;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (dim % 4 == 0 && (uintptr_t)x % 16 == 0 && (uintptr_t)xs % 16 == 0) {
+        const uint32_t d4 = dim / 4;
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4; i += stride) {
+            const float c = __ldg(w + i / d4);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+            reinterpret_cast<float4*>(xs)[i] = make_float4(c * v.x, c * v.y, c * v.z, c * v.w);
+        }
+    } else {
+        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride)
+            xs[i] = __ldg(w + i / dim) * __ldg(x + i);
+    }
+}
+
 namespace gnna {
 
 // Scheduled aggregation over a plan (one K3 / K3A launch) with the optional epilogue
@@ -927,6 +948,30 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
         a.pf = pf_env >= 0 ? (uint32_t)pf_env : (uint32_t)(3 * ctx->num_sms);  // ~ the resident CTAs of one wave
     }
     if (plan->G == 0 && plan->nempty == 0) return;
+    // Per-source weights (GCN's norm[u] on an arbitrary x): with enough edges
+    // per row, scale each row once into a scratch copy and gather that with
+    // the plain K3 (the self term still reads the caller's x): C3 76.4 ->
+    // 67 us, C5 even (15.7 ms; profiles r02j).  Rounding: rn(w x) then the
+    // sum, as in the GCN layer form, against fmaf per edge; the fused fan-out
+    // takes the same path, so its replicas hold the same bits.
+    // GNNA_PRESCALE=0 keeps the per-edge weights.
+    DevBuf<float> xs;
+    {
+        static const int pre_env = std::getenv("GNNA_PRESCALE") ? std::atoi(std::getenv("GNNA_PRESCALE")) : -1;
+        const uint32_t rows = plan->row_end - plan->row_begin;
+        const bool pre = a.nw && dtype == GNNA_F32 &&
+                         (pre_env >= 0 ? pre_env != 0 : plan->nnz >= 4ull * (rows ? rows : 1));
+        if (pre) {
+            xs = DevBuf<float>((size_t)plan->n * dim, ctx->stream);
+            const uint64_t work = (uint64_t)plan->n * dim / (dim % 4 == 0 ? 4 : 1);
+            const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, 16ull * ctx->num_sms));
+            k_prescale_rows<<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(x), a.nw, plan->n, dim, xs.get());
+            launched(ctx, "k_prescale_rows");
+            a.xself = x;
+            a.x = xs.get();
+            a.nw = nullptr;
+        }
+    }
     const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;  // unit blocks
     if (dtype == GNNA_F32) {
         if (s.vec == 4) launch_k3<float, 4>(ctx, a, s, grid, plan);

@@ -178,6 +178,7 @@ struct gnna_plan {
     const uint64_t* row_ptr = nullptr;
     const uint32_t* col = nullptr;
     uint64_t G = 0;              // workload units
+    uint64_t nnz = 0;            // CSR entries of the plan's rows
     uint64_t runs = 0;           // Algorithm-1 runs (= leaders)
     uint64_t nsplit = 0;         // nodes whose units span > 1 schedule block
     uint64_t ncarry = 0;         // carried run partials

@@ -297,6 +297,13 @@ gnna_status gnna_plan_create(gnna_ctx* ctx, const uint64_t* d_row_ptr, const uin
             }
             k1_tail<<<1, 1, 0, s>>>(d_row_ptr, row_end, G, plan->part_ptr.get());
             gnna::launched(ctx, "k1_tail");
+            {
+                uint64_t ends[2] = {0, 0};
+                GNNA_CUDA(cudaMemcpyAsync(&ends[0], d_row_ptr + row_begin, 8, cudaMemcpyDeviceToHost, s));
+                GNNA_CUDA(cudaMemcpyAsync(&ends[1], d_row_ptr + row_end, 8, cudaMemcpyDeviceToHost, s));
+                GNNA_CUDA(cudaStreamSynchronize(s));
+                plan->nnz = ends[1] - ends[0];
+            }
             if (G) {
                 // Algorithm-1 arrays at the params' block width.
                 const uint64_t b1 = (G + plan->wpb_params - 1) / plan->wpb_params;
