@@ -951,11 +951,13 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
     // Per-source weights (GCN's norm[u] on an arbitrary x): with enough edges
     // per row, scale each row once into a scratch copy and gather that with
     // the plain K3 (the self term still reads the caller's x): C3 76.4 ->
-    // 67 us, C5 even (15.7 ms; profiles r02j).  Rounding: rn(w x) then the
+    // 66.5 us, C5 15.7 -> 14.4 ms (profiles r02j).  Rounding: rn(w x) then the
     // sum, as in the GCN layer form, against fmaf per edge; the fused fan-out
     // takes the same path, so its replicas hold the same bits.
     // GNNA_PRESCALE=0 keeps the per-edge weights.
     DevBuf<float> xs;
+    bool window_moved = false;
+    cudaStreamAttrValue window_saved{};
     {
         static const int pre_env = std::getenv("GNNA_PRESCALE") ? std::atoi(std::getenv("GNNA_PRESCALE")) : -1;
         const uint32_t rows = plan->row_end - plan->row_begin;
@@ -970,8 +972,34 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
             a.xself = x;
             a.x = xs.get();
             a.nw = nullptr;
+            // an L2 persisting window the caller set on rows of x (gnna_set_l2_window) follows
+            // the gather to the same rows of the scaled copy for this launch
+            cudaStreamAttrValue w{};
+            if (cudaStreamGetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &w) == cudaSuccess) {
+                const auto* lo = static_cast<const unsigned char*>(x);
+                const auto* bp = static_cast<const unsigned char*>(w.accessPolicyWindow.base_ptr);
+                const size_t xbytes = (size_t)plan->n * dim * sizeof(float);
+                if (w.accessPolicyWindow.num_bytes && bp >= lo && bp < lo + xbytes) {
+                    window_saved = w;
+                    cudaStreamAttrValue moved = w;
+                    moved.accessPolicyWindow.base_ptr = reinterpret_cast<unsigned char*>(xs.get()) + (bp - lo);
+                    moved.accessPolicyWindow.num_bytes = std::min<size_t>(w.accessPolicyWindow.num_bytes, xbytes - (bp - lo));
+                    GNNA_CUDA(cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &moved));
+                    window_moved = true;
+                }
+            } else {
+                cudaGetLastError();
+            }
         }
     }
+    struct RestoreWindow {
+        gnna_ctx* ctx;
+        const bool& moved;
+        cudaStreamAttrValue& saved;
+        ~RestoreWindow() {
+            if (moved) cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &saved);
+        }
+    } restore{ctx, window_moved, window_saved};
     const uint64_t grid = plan->G ? (plan->G + a.upc - 1) / a.upc : 0;  // unit blocks
     if (dtype == GNNA_F32) {
         if (s.vec == 4) launch_k3<float, 4>(ctx, a, s, grid, plan);

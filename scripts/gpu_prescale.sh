@@ -1,4 +1,5 @@
-# GCN gather form: per-source weights applied by a row pre-scale pass + plain K3 (default) vs per-edge weights (GNNA_PRESCALE=0)
+# GCN gather form: per-source weights applied by a row pre-scale pass + plain K3 (default) vs per-edge weights (GNNA_PRESCALE=0);
+# the caller's L2 window on x follows to the scaled copy (C5's hub rows)
 set -x
 timeout 1200 python -m pytest tests -m gpu -q -x --timeout 900 -k "gcn or weight or c3 or configs or fanout or layers or model" 2>&1 | tail -1
 for rep in 1 2; do
