@@ -705,6 +705,7 @@ def headline_forms(ctx, plan, rp, col, x, y, args, n, dim, rows, nnz):
         forms["gcn_layer"] = (lambda: plan.aggregate_ex(xs, out=y, row_scale=rs), 4 * rows,
                               "GCN layer form: x pre-scaled by norm in the update GEMM's epilogue, "
                               "K3 = plain sum + destination scale")
+        FORM_SRC["gcn_layer"] = xs
     if args.extras_c5 and args.agg == "sum":
         x64 = x.double()
         y64 = torch.empty_like(x64)
@@ -712,7 +713,25 @@ def headline_forms(ctx, plan, rp, col, x, y, args, n, dim, rows, nnz):
         forms["sum_f64"] = (lambda: plan.aggregate(x64, out=y64), bf,
                             "aggregate_scheduled in fp64 (the reference's precision; bitwise its tree)")
         forms["sum_f64"] += (y64,)
+        FORM_SRC["sum_f64"] = x64
     return forms
+
+
+# The tensor each headline form gathers from, when it is not x: the hub L2
+# window (the same byte budget) is set on ITS front rows while that form runs
+# -- what an application does for the buffer it aggregates -- then moved
+# back to x.  Moving it first clears the persisting lines of the old window.
+FORM_SRC = {}
+
+
+def form_window(ctx, S, name):
+    """Point the hub L2 window at the rows form `name` gathers (no-op when
+    the headline did not pin)."""
+    if not S["l2_pin"].get("pinned"):
+        return
+    src = FORM_SRC.get(name, S["x"])
+    ctx.set_l2_window(None, 0)
+    ctx.pin_hot_rows(S["rp_host"], src, cap_bytes=S["l2_pin"]["cap_MB"] << 20)
 
 
 def setup_headline(args, ctx, dev, world, rank):
@@ -773,7 +792,9 @@ def probe_main(ctx, dev, args):
     S = setup_headline(args, ctx, dev, 1, 0)
     win = ProbeWindow(ctx, args.probe_out)
     for name, form in S["forms"].items():
+        form_window(ctx, S, name)
         win.capture(name, form[0])
+    form_window(ctx, S, "sum")
     win.close()
 
 
@@ -890,13 +911,15 @@ def run_ours(args):
             yout = form[3] if len(form) > 3 else y
             if name == args.agg:
                 continue
+            form_window(ctx, S, name)
             t = time_calls(call, max(5, min(args.steps, 10)), None, stream) * 1e-3
+            form_window(ctx, S, args.agg)
             bb = synth.b_alg(r1 - r0, S["my_nnz"], cfg.dim) + xb
             c5_extras.append({"case": f"c5/{name}", "workload": cfg.name, "aggregation": name, "form": desc,
                               "n": n, "nnz": nnz, "dim": cfg.dim, "kernel_ms": t * 1e3,
                               "edge_dim_per_s": nnz * cfg.dim / t, "algorithmic_bytes": bb,
                               "effective_GBps": bb / t / 1e9, "effective_frac_of_measured_hbm": bb / t / 1e9 / peak,
-                              "l2": "inputs > L2; hub L2 window as the headline",
+                              "l2": "inputs > L2; hub L2 window on the same front rows of the gathered tensor",
                               "dtype": "f64" if name.endswith("f64") else "f32",
                               "parity": spot_check(rp_host, col, x, yout, [(r0, r1)], cfg.dim,
                                                    agg="sum" if name == "sum_f64" else name,
