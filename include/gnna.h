@@ -165,7 +165,13 @@ GNNA_API gnna_status gnna_aggregate(gnna_ctx* ctx, const gnna_plan* plan, int dt
  * node_weight is per source node (F32 only; NULL = all ones; GCN: norm);
  * self_weight NULL uses the constant alpha (0 = no self term); row_scale NULL
  * = 1; mask (same shape/dtype as y) zeroes y where mask <= 0 (ReLU backward).
- * dim 0 = the plan's params.dim; any other width reuses the plan's schedule. */
+ * dim 0 = the plan's params.dim; any other width reuses the plan's schedule.
+ * With node weights and >= 4 edges per row, x is first scaled row by row into
+ * a stream-ordered scratch copy (n x dim floats) that the gather reads; the
+ * self term still reads x, and an L2 access-policy window on ctx's stream that
+ * covers rows of x is moved to the same rows of the copy for the launch.  Each
+ * term is then rn(node_weight[u] * x[u]) added in CSR order (the GCN layer's
+ * rounding), instead of one fmaf per edge (GNNA_PRESCALE=0). */
 typedef struct {
     uint32_t dim;
     const float* node_weight;
@@ -192,8 +198,10 @@ GNNA_API gnna_status gnna_aggregate_ex(gnna_ctx* ctx, const gnna_plan* plan, int
  * The caller orders the peers' reads after every rank's kernel (a stream-
  * ordered cross-rank barrier), and this rank's stores after the peers'
  * reads of the previous contents.  Rows outside the plan are never written.
- * Node weights (opts->node_weight: GCN's gathered norm[u]) are supported on
- * fp32 rows of at most one 16-byte chunk per lane (d <= 128). */
+ * Node weights (opts->node_weight: GCN's gathered norm[u]) take the pre-scaled
+ * gather of gnna_aggregate_ex (any width; the replicas get the same bits); with
+ * GNNA_PRESCALE=0 or < 4 edges per row, only fp32 rows of at most one 16-byte
+ * chunk per lane (GNNA_ERR_DOMAIN otherwise). */
 #define GNNA_MAX_PEERS 7
 GNNA_API gnna_status gnna_aggregate_fanout(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim_mode,
                                            const void* d_x, void* d_y, const gnna_agg_opts* opts,
