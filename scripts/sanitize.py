@@ -124,6 +124,31 @@ def main():
         got = pe.aggregate_ex(xs, alpha=0.5)
         want = orc.aggregate_oracle(rpe, cole, xs.double().cpu().numpy()) + 0.5 * xs.double().cpu().numpy()
         assert np.allclose(got.double().cpu().numpy(), want, rtol=1e-5)
+    # round 2, late: the split-role X.W kernel (K 128), the packed / 128-row dW
+    # kernel, the pre-scaled weighted gather (node weights, >= 4 edges per row)
+    # and the staged pageable copies (pinned bounce ring)
+    for k, q in ((128, 32), (96, 16)):
+        a = dev(rng.random((5000, k)) - 0.5).float()
+        wq = dev(rng.random((k, q)) - 0.5).float()
+        assert torch.allclose(ctx.gemm(a, wq).double(), a.double() @ wq.double(), rtol=1e-4, atol=1e-4)
+        g = dev(rng.random((5000, q)) - 0.5).float()
+        assert torch.allclose(ctx_gemm_tn(ctx, a, g).double(), a.double().t() @ g.double(), rtol=1e-4, atol=1e-3)
+    pw = ctx.plan(drp, dcol, Params.make(ngs=16, dw=16, tpb=256, dim=32), 2)
+    yw = pw.aggregate_ex(xf, node_weight=rs, self_weight=sw, row_scale=rs)
+    deg = np.diff(rp).astype(np.float64)
+    x64 = xf.double().cpu().numpy()
+    nrm = rs.double().cpu().numpy()
+    swn = sw.double().cpu().numpy()
+    want = orc.aggregate_oracle(rp, col, x64 * nrm[:, None]) + swn[:, None] * x64
+    assert np.allclose(yw.double().cpu().numpy(), nrm[:, None] * want, rtol=1e-5, atol=1e-6), deg.mean()
+    big = np.frombuffer(rng.bytes((9 << 20) + 20), dtype=np.uint8).copy()
+    dbig = torch.empty(big.size, dtype=torch.uint8, device="cuda")
+    assert ctx.L.gnna_copy_to_device(ctx.h, C.c_void_p(dbig.data_ptr()), C.c_void_p(big.ctypes.data),
+                                     C.c_size_t(big.size)) == 0
+    back = np.empty_like(big)
+    assert ctx.L.gnna_copy_to_host(ctx.h, C.c_void_p(back.ctypes.data), C.c_void_p(dbig.data_ptr()),
+                                   C.c_size_t(big.size)) == 0
+    assert np.array_equal(back, big)
     torch.cuda.synchronize()
     print("sanitize workload ok")
 
