@@ -144,8 +144,8 @@ class GCN2:
         return dw1, dw2
 
     def sgd(self, dw1, dw2):
-        self.w1.add_(dw1, alpha=-self.lr)  # one fused kernel per weight
-        self.w2.add_(dw2, alpha=-self.lr)
+        # both weights in one multi-tensor kernel (w += (-lr) * dw, as add_ per weight)
+        torch._foreach_add_([self.w1, self.w2], [dw1, dw2], alpha=-self.lr)
 
     def step(self, x, dy):
         y = self.forward(x)
