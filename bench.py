@@ -1061,7 +1061,7 @@ def run_e2e(ctx, rp, col, x, p, r0, r1, cfg, args, world, dev):
     h_x = x.cpu().pin_memory()
     rows = r1 - r0
     h_y = torch.empty((rows, cfg.dim), dtype=torch.float32).pin_memory()
-    steps = max(2, args.steps)  # one pipelined stream of K batches: fill and drain amortised over the run
+    steps = max(20, args.steps)  # one pipelined stream of >= 20 batches: fill and drain amortised over the run
 
     # one synchronous call (upload, plan, K3, download back to back)
     ctx.aggregate_host_rows(h_rp, h_col, h_x, p, r0, r1, h_y)
