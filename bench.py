@@ -1087,39 +1087,56 @@ def run_e2e(ctx, rp, col, x, p, r0, r1, cfg, args, world, dev):
     nnz = int(col.numel())
     h2d = h_rp.numel() * 8 + h_col.numel() * 4 + h_x.numel() * 4
     d2h = h_y.numel() * 4
-    duplex = pcie_duplex_gbps()
-    floor_ms = (h2d + d2h) / (duplex * 1e9) * 1e3 if duplex else None
+    duplex, up_gbps, down_gbps = pcie_duplex_gbps(per_direction=True)
+    # each direction is its own resource: the step cannot beat the slower side
+    floor_ms = max(h2d / (up_gbps * 1e9), d2h / (down_gbps * 1e9)) * 1e3 if up_gbps and down_gbps else None
+    floor_sum_ms = (h2d + d2h) / (duplex * 1e9) * 1e3 if duplex else None
     return {"value": nnz * cfg.dim / t, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": t * 1e3, "steps": steps, "reps_ms_per_step": [round(r * 1e3, 1) for r in reps],
             "single_call_ms": single * 1e3,
-            "pcie_duplex_GBps_measured": duplex, "pcie_floor_ms_per_step": floor_ms,
+            "pcie_duplex_GBps_measured": duplex, "pcie_h2d_GBps_under_duplex": up_gbps,
+            "pcie_d2h_GBps_under_duplex": down_gbps,
+            "pcie_floor_ms_per_step": floor_ms,  # max over directions of bytes / that direction's duplex rate
+            "pcie_floor_sum_ms_per_step": floor_sum_ms,  # (H2D + D2H) / total duplex rate (looser)
             "path": "gnna_aggregate_host_stream (C-ABI, pinned host buffers; per batch: CSR slice + features "
                     "upload, plan, K3, rows download; batches pipelined)"}
 
 
-def pcie_duplex_gbps(gb=1):
+def pcie_duplex_gbps(gb=1, per_direction=False):
     """Measured full-duplex pinned copy bandwidth (H2D and D2H at once on two
-    streams, GB/s total): the floor of the e2e step, whose copies overlap."""
+    streams): GB/s total, or with per_direction the (H2D, D2H) rates each
+    direction sustains while the other runs (CUDA events per stream) -- the
+    floor of the e2e step, whose copies overlap."""
     import torch
     try:
         n = gb * (1 << 30) // 4
         h, h2 = torch.empty(n).pin_memory(), torch.empty(n).pin_memory()
         d, d2 = torch.empty(n, device="cuda"), torch.empty(n, device="cuda")
         s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
         def both():
             with torch.cuda.stream(s1):
+                ev[0].record(s1)
                 d.copy_(h, non_blocking=True)
+                ev[1].record(s1)
             with torch.cuda.stream(s2):
+                ev[2].record(s2)
                 h2.copy_(d2, non_blocking=True)
+                ev[3].record(s2)
         both()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         both()
         torch.cuda.synchronize()
-        return round(2 * n * 4 / (time.perf_counter() - t0) / 1e9, 1)
+        total = round(2 * n * 4 / (time.perf_counter() - t0) / 1e9, 1)
+        if not per_direction:
+            return total
+        h2d = n * 4 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
+        d2h = n * 4 / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9
+        return total, round(h2d, 1), round(d2h, 1)
     except Exception:
-        return None
+        return (None, None, None) if per_direction else None
 
 
 def run_train_sharded(args):
