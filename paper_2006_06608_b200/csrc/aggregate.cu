@@ -916,6 +916,18 @@ void aggregate_plan_fan(gnna_ctx* ctx, const gnna_plan* plan, int dtype, int dim
     a.cidx = plan->cidx.get();
     a.units = plan->G;
     a.upc = ((256 / s.team) / wpb) * wpb;
+    {
+        // at most 32 units per CTA: for narrow teams (d 16 fp32: 4 lanes) a
+        // 256-thread CTA held 64 units and lived as long as the longest; 128
+        // threads trim that tail (C3 sum 53.4 -> 52.7 us, train step 0.331 ->
+        // 0.324 ms; C4 / C5 unchanged).  GNNA_K3_UPC_MAX=0 restores 256
+        // threads, other values cap.
+        static const int upc_max = [] {
+            const char* e = std::getenv("GNNA_K3_UPC_MAX");
+            return e && *e ? std::atoi(e) : 32;
+        }();
+        if (upc_max > 0) a.upc = std::min<uint32_t>(a.upc, std::max<uint32_t>(wpb, ((uint32_t)upc_max / wpb) * wpb));
+    }
     a.row_ptr = plan->row_ptr;
     a.col = plan->col;
     a.x = x;
