@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(256, K3A_MINB) k3a_aggregate(AggArgs a) {
     }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     VT* sm = reinterpret_cast<VT*>(smem_raw);   // [upc][TEAM] staged partials
-    VT* gbuf = sm + 256 + (threadIdx.x / 32) * (K3A_ROWS * 32);  // this warp's gather slots
+    VT* gbuf = sm + blockDim.x + (threadIdx.x / 32) * (K3A_ROWS * 32);  // this warp's gather slots
     const uint32_t tu = threadIdx.x / TEAM, lane = threadIdx.x % TEAM;
     const uint64_t u = (uint64_t)blockIdx.x * a.upc + tu;
     const bool active = tu < a.upc && u < a.units;
@@ -734,15 +734,16 @@ Shape choose_shape(int elem, uint32_t dim, uint32_t dw, uint32_t team_cap, const
 
 // K3A launch (cp.async row gather into shared memory): true when it ran.
 template <class T, int VEC, int TEAM, bool EW, bool FAN>
-void launch_k3a_v(gnna_ctx* ctx, AggArgs& a, uint64_t grid) {
+void launch_k3a_v(gnna_ctx* ctx, AggArgs& a, uint64_t grid, unsigned threads) {
     auto kern = k3a_aggregate<T, VEC, TEAM, EW, FAN>;
-    const size_t smem = (256 + 8 * K3A_ROWS * 32) * sizeof(Vec<T, VEC>);
+    const size_t smem = (threads + (threads / 32) * K3A_ROWS * 32) * sizeof(Vec<T, VEC>);
     static bool attr = false;
-    if (!attr) {
-        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!attr) {  // the 256-thread size bounds every smaller one
+        GNNA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)((256 + 8 * K3A_ROWS * 32) * sizeof(Vec<T, VEC>))));
         attr = true;
     }
-    kern<<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
+    kern<<<(unsigned)grid, threads, smem, ctx->stream>>>(a);
     gnna::launched(ctx, "k3a_aggregate");
 }
 
@@ -782,11 +783,23 @@ void launch_k3_team(gnna_ctx* ctx, AggArgs& a, uint32_t kmax, uint64_t grid, con
     a.split_count = plan->fix_count.get();
     if (k3a_applies<T, VEC, TEAM>(a, kmax)) {
         if constexpr (TEAM >= 2 && TEAM <= 8 && sizeof(T) * VEC == 16) {
-            const uint64_t total = grid + (a.nempty + 256 / TEAM - 1) / (256 / TEAM);
+            // 8 units per K3A CTA (64 threads for fp64 d 16): C3 fp64 0.093 ->
+            // 0.088 ms (16: 0.089); GNNA_K3A_UPC=0 keeps K3's units per CTA
+            static const int k3a_upc = [] {
+                const char* e = std::getenv("GNNA_K3A_UPC");
+                return e && *e ? std::atoi(e) : 8;
+            }();
+            if (k3a_upc > 0 && (uint32_t)k3a_upc < a.upc) {
+                a.upc = std::max<uint32_t>(plan->wpb, ((uint32_t)k3a_upc / plan->wpb) * plan->wpb);
+                grid = (plan->G + a.upc - 1) / a.upc;
+                a.unit_blocks = grid;
+            }
+            const unsigned threads = (a.upc * TEAM + 31) / 32 * 32;
+            const uint64_t total = grid + (a.nempty + threads / TEAM - 1) / (threads / TEAM);
             if (total > 0x7fffffffull) gnna::raise(GNNA_ERR_DOMAIN, "aggregate: grid too large");
-            if (fan) launch_k3a_v<T, VEC, TEAM, false, true>(ctx, a, total);
-            else if (a.nw && kEW) launch_k3a_v<T, VEC, TEAM, kEW, false>(ctx, a, total);
-            else launch_k3a_v<T, VEC, TEAM, false, false>(ctx, a, total);
+            if (fan) launch_k3a_v<T, VEC, TEAM, false, true>(ctx, a, total, threads);
+            else if (a.nw && kEW) launch_k3a_v<T, VEC, TEAM, kEW, false>(ctx, a, total, threads);
+            else launch_k3a_v<T, VEC, TEAM, false, false>(ctx, a, total, threads);
         }
         return;
     }
