@@ -948,7 +948,10 @@ void launch_tc_n(gnna_ctx* ctx, const TcArgs& g) {
 //   * per K step: A_hi x [B_hi | B_lo] (SS, columns [0,32QS) and
 //     [32QS,64QS)) + A_lo x B_hi (TS, onto [0,32QS)), accumulated in TMEM
 //     for the CTA's whole run of BK-row blocks (split-K); the epilogue adds
-//     the two column halves.
+//     the two column halves (packed QS = 0 below: both MMAs are N = 32 over
+//     the one [B_hi | B_lo] slice, so A_lo x B_lo lands in columns 16-31 too);
+//   * warp 4 issues the MMAs, warp 5 (PROD) refills each stage as its MMAs
+//     commit, warps 0-3 convert.
 // M = 128 reads 4 A slices from the stage base: the 4 - PS phantom slices
 // alias the following bytes (in bounds) and only feed discarded rows of D.
 // Per-CTA partials are summed by k_reduce_partials in a fixed slice order
