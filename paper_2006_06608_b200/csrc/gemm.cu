@@ -1003,8 +1003,7 @@ void launch_dense_bwd(gnna_ctx* ctx, const float* dy, const float* w, const floa
     gnna::DevBuf<float> part((size_t)ctas * P * Q, ctx->stream);
     k6_dense_bwd<P, Q><<<ctas, 256, sbytes, ctx->stream>>>(dy, w, z, rs, m, rpc, dz, part.get());
     gnna::launched(ctx, "k6_dense_bwd");
-    gnna::k_reduce_partials<<<(P * Q + 31) / 32, 1024, 0, ctx->stream>>>(part.get(), ctas, P * Q, dw);
-    gnna::launched(ctx, "k_reduce_partials");
+    gnna::reduce_partials(ctx, part.get(), ctas, P * Q, dw);
 }
 
 constexpr int TN4_ROWS = 32;

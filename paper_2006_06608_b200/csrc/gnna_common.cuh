@@ -165,6 +165,16 @@ __global__ void __launch_bounds__(32 * SLICES) k_reduce_partials(const float* __
     }
 }
 
+// The same sum for few outputs over many chunks (the C3 dense backward:
+// 352 outputs x ~600 CTA partials): 8 outputs x 128 chunk slices per block,
+// so the grid has 4x the blocks and each slice's dependent chain is 4x
+// shorter; slice 0 adds the 128 slice sums in slice order (fixed order).
+__global__ void __launch_bounds__(1024) k_reduce_partials_narrow(const float* __restrict__ part, uint32_t chunks,
+                                                                uint32_t total, float* __restrict__ out);
+
+// Launches the better of the two reducers for (chunks, total).
+void reduce_partials(gnna_ctx* ctx, const float* part, uint32_t chunks, uint32_t total, float* out);
+
 }  // namespace gnna
 
 // Internal plan (gnna_plan is opaque at the ABI).

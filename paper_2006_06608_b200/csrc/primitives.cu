@@ -94,3 +94,42 @@ void sort_keys_u64(gnna_ctx* ctx, uint64_t* keys, uint64_t count, int end_bit) {
 }
 
 }  // namespace gnna
+
+namespace gnna {
+
+__global__ void __launch_bounds__(1024) k_reduce_partials_narrow(const float* __restrict__ part, uint32_t chunks,
+                                                                uint32_t total, float* __restrict__ out) {
+    constexpr uint32_t OUTS = 8, SLICES = 128;
+    __shared__ float red[SLICES][OUTS + 1];
+    const uint32_t tx = threadIdx.x % OUTS, sl = threadIdx.x / OUTS;
+    const uint32_t o = blockIdx.x * OUTS + tx;
+    float s = 0.f;
+    if (o < total) {
+#pragma unroll 4
+        for (uint32_t c = sl; c < chunks; c += SLICES) s += part[(size_t)c * total + o];
+    }
+    red[sl][tx] = s;
+    __syncthreads();
+    if (sl == 0 && o < total) {
+        float t = 0.f;
+        for (uint32_t i = 0; i < SLICES; ++i) t += red[i][tx];
+        out[o] = t;
+    }
+}
+
+void reduce_partials(gnna_ctx* ctx, const float* part, uint32_t chunks, uint32_t total, float* out) {
+    static const int mode = [] {
+        const char* e = std::getenv("GNNA_REDUCE_NARROW");  // A/B switch: 0 / 1 force either reducer
+        return e && *e ? std::atoi(e) : -1;
+    }();
+    const bool narrow = mode >= 0 ? mode != 0 : ((total + 31) / 32 < (uint32_t)ctx->num_sms / 2 && chunks >= 256);
+    if (narrow) {
+        k_reduce_partials_narrow<<<(total + 7) / 8, 1024, 0, ctx->stream>>>(part, chunks, total, out);
+        launched(ctx, "k_reduce_partials_narrow");
+    } else {
+        k_reduce_partials<<<(total + 31) / 32, 1024, 0, ctx->stream>>>(part, chunks, total, out);
+        launched(ctx, "k_reduce_partials");
+    }
+}
+
+}  // namespace gnna
